@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json metric on B200: per-kernel GB/s or TFLOP/s vs the
+B200 roofline, and task-graph time at 1/2/4/8 GPUs.
+
+A STEP is one execute+sync of the "jacc-suite" task graph: every row of
+SURVEY §8(a) at BASELINE.json's full sizes, sharded over the ranks where the
+path shards:
+  cfg1  vadd(a, b -> c) -> reduce(c -> s)            n = 2^20   (+ allreduce s)
+  cfg2  histogram(keys -> bins[256])                  n = 2^28   (+ allreduce bins)
+  cfg3  Black-Scholes(u -> call, put)                 n = 2^26
+  cfg4  SGEMM C = A.B (3xTF32, tcgen05)               8192^3     (row blocks)
+  cfg5  10 x N-body step (2^17 bodies)                           (+ allgather pos)
+value = task graphs per second for the whole job (strong scaling: the total
+work per graph is fixed), inputs resident in HBM, device time from CUDA
+events (max over ranks), L2 flushed (256 MiB write) before every timed step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl jacc|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "per-kernel GB/s or GFLOP/s vs B200 roofline; task-graph time at 1/2/4/8 GPU"
+UNIT = "task-graphs/s"
+WORKLOAD = ("jacc-suite: cfg1 vadd+reduce 2^20 f32, cfg2 histogram 2^28 i32 -> 256 bins, cfg3 Black-Scholes "
+            "2^26 f32, cfg4 SGEMM 8192^3 f32 (3xTF32 tcgen05), cfg5 N-body 2^17 bodies x 10 steps; one "
+            "task graph per step")
+NBODY_FLOP = 20   # conventional flops per body-body interaction
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def fp32_alu_tflops(mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x clock
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------ distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, world
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), p[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        smax = max(r[1] for r in rows)
+        load = [r for r in rows if r[0] > 0.5 * smax] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[2]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------ the suite graph
+class Suite:
+    """The per-rank jacc-suite task graph (device-resident or host-buffer form)."""
+
+    def __init__(self, torch, J, jacc, rank, world, comm_ptr, host_mode=False, sgemm_mode=0):
+        from paper_1508_06791_b200.torch_glue import make_graph
+        self.torch, self.J = torch, J
+        self.rank, self.world = rank, world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.g, self.streams = make_graph(dev.index, n_streams=4, rank=rank, world=world, nccl_comm=comm_ptr)
+        g = self.g
+        R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
+        self.tasks = {}     # name -> list of task ids
+        self.units = {}     # name -> algorithmic bytes or flops per launch
+        keep = []
+
+        def put(x):
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            t = t.pin_memory() if host_mode else t.to(dev)
+            keep.append(t)
+            return t
+
+        def empty(shape, dtype):
+            t = torch.empty(shape, dtype=dtype, pin_memory=host_mode) if host_mode else \
+                torch.empty(shape, dtype=dtype, device=dev)
+            keep.append(t)
+            return t
+
+        def task(name, op, args, params=None):
+            tid = g.add_task(op, args, params)
+            self.tasks.setdefault(name, []).append(tid)
+            return tid
+
+        # cfg1: vadd -> reduce (+ allreduce of the partial sum)
+        n1 = synth.CFG1_N
+        lo, hi = synth.shard_range(n1, rank, world)
+        a, b = synth.vadd_inputs(n1)
+        da, db = put(a[lo:hi]), put(b[lo:hi])
+        dc, ds = empty(hi - lo, torch.float32), empty(1, torch.float32)
+        task("vadd", J.JACC_OP_VADD_F32, [g.a(da, R), g.a(db, R), g.a(dc, W)])
+        task("reduce", J.JACC_OP_REDUCE_SUM_F32, [g.a(dc, R), g.a(ds, W)])
+        self.units["vadd"] = 12 * (hi - lo)
+        self.units["reduce"] = 4 * (hi - lo)
+        if world > 1:
+            task("allreduce_s", J.JACC_OP_ALLREDUCE_SUM, [g.a(ds, RW)])
+        # cfg2: histogram (+ allreduce of the bins)
+        n2 = synth.CFG2_N
+        lo, hi = synth.shard_range(n2, rank, world)
+        keys = synth.hist_keys(n2)
+        dk = put(keys[lo:hi])
+        del keys
+        dbins = empty(256, torch.int32)
+        task("hist", J.JACC_OP_HISTOGRAM_I32, [g.a(dk, R), g.a(dbins, W)], jacc.jacc_hist_params_t(256))
+        self.units["hist"] = 4 * (hi - lo)
+        if world > 1:
+            task("allreduce_bins", J.JACC_OP_ALLREDUCE_SUM, [g.a(dbins, RW)])
+        # cfg3: Black-Scholes
+        n3 = synth.CFG3_N
+        lo, hi = synth.shard_range(n3, rank, world)
+        u = synth.bs_rand(n3)
+        du = put(u[lo:hi])
+        del u
+        dcall, dput = empty(hi - lo, torch.float32), empty(hi - lo, torch.float32)
+        task("bs", J.JACC_OP_BLACKSCHOLES_F32, [g.a(du, R), g.a(dcall, W), g.a(dput, W)])
+        self.units["bs"] = 12 * (hi - lo)
+        # cfg4: SGEMM row blocks, B replicated
+        n4 = synth.CFG4_MNK
+        lo, hi = synth.shard_range(n4, rank, world)
+        A, B = synth.sgemm_inputs(n4, n4, n4)
+        dA, dB = put(A[lo:hi]), put(B)
+        del A, B
+        dC = empty((hi - lo, n4), torch.float32)
+        task("sgemm", J.JACC_OP_SGEMM_F32, [g.a(dA, R), g.a(dB, R), g.a(dC, W)],
+             jacc.jacc_sgemm_params_t(hi - lo, n4, n4, n4, n4, n4, sgemm_mode, 0))
+        self.units["sgemm"] = 2 * (hi - lo) * n4 * n4
+        # cfg5: N-body, 10 steps (+ all-gather of positions per step)
+        n5 = synth.CFG5_N
+        lo, hi = synth.shard_range(n5, rank, world)
+        pos, vel = synth.nbody_state(n5)
+        prm = jacc.jacc_nbody_params_t(lo if world > 1 else 0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G)
+        if world == 1:
+            P = [put(pos), empty(pos.shape, torch.float32)]
+            V = put(vel)
+            for k in range(synth.CFG5_STEPS):
+                task("nbody", J.JACC_OP_NBODY_STEP_F32,
+                     [g.a(P[k % 2], R, f32x4=True), g.a(V, RW, f32x4=True), g.a(P[(k + 1) % 2], W, f32x4=True)],
+                     prm)
+        else:
+            L = [put(pos[lo:hi]), empty((hi - lo, 4), torch.float32)]
+            V = put(vel[lo:hi])
+            ALL = torch.empty((n5, 4), dtype=torch.float32, device=dev)   # DEVICE temp, never transferred
+            keep.append(ALL)
+            for k in range(synth.CFG5_STEPS):
+                task("allgather_pos", J.JACC_OP_ALLGATHER, [g.a(L[k % 2], R, f32x4=True), g.a(ALL, W, f32x4=True)])
+                task("nbody", J.JACC_OP_NBODY_STEP_F32,
+                     [g.a(ALL, R, f32x4=True), g.a(V, RW, f32x4=True), g.a(L[(k + 1) % 2], W, f32x4=True)], prm)
+        self.units["nbody"] = NBODY_FLOP * (hi - lo) * n5
+        self.keep = keep
+
+    def all_streams(self):
+        s = self.streams
+        return list(s["compute"]) + [s["h2d"], s["d2h"], s["comm"]]
+
+    def timed_step(self, flush_buf):
+        """One execute+sync; device time (ms) from an event all graph streams
+        wait on to the last event recorded on any graph stream."""
+        torch = self.torch
+        flush_buf.fill_(1.0)          # evict L2 (256 MiB write), outside the timed window
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        e0.record(cur)
+        for s in self.all_streams():
+            s.wait_event(e0)
+        self.g.execute()
+        ends = []
+        for s in self.all_streams():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            ends.append(e)
+        self.g.sync()
+        torch.cuda.synchronize()
+        return max(e0.elapsed_time(e) for e in ends)
+
+    def task_times(self):
+        return {name: [self.g.task_ms(t) for t in ids] for name, ids in self.tasks.items()}
+
+
+def kernel_report(times, units, peaks, clocks_mhz=None):
+    """Per-kernel achieved vs roofline from per-launch CUDA-event durations."""
+    hbm = peaks["hbm_gbs"]
+    tf32_3x = peaks["bf16_tflops"] * 0.5 / 3.0       # TF32 = bf16 x 1/2 (nominal ratio); 3 MMAs per product
+    alu = fp32_alu_tflops(peaks["sm_max_mhz"])
+    out = {}
+    for name, ts in times.items():
+        if name not in units or not ts:
+            continue
+        ms = statistics.mean(ts)
+        if name in ("vadd", "reduce", "hist", "bs"):
+            ach = units[name] / (ms * 1e-3) / 1e9
+            out[name] = {"bound": "hbm", "ms": ms, "achieved": ach, "unit": "GB/s", "peak": hbm, "frac": ach / hbm,
+                         "bytes_per_launch": units[name], "launches": len(ts)}
+        elif name == "sgemm":
+            ach = units[name] / (ms * 1e-3) / 1e12
+            out[name] = {"bound": "tensor", "ms": ms, "achieved": ach, "unit": "TFLOP/s", "peak": tf32_3x,
+                         "frac": ach / tf32_3x, "flop_per_launch": units[name], "launches": len(ts),
+                         "peak_note": "3xTF32 ceiling = measured bf16 x 0.5 (tf32/bf16 nominal) / 3 MMAs"}
+        elif name == "nbody":
+            ach = units[name] / (ms * 1e-3) / 1e12
+            out[name] = {"bound": "alu", "ms": ms, "achieved": ach, "unit": "TFLOP/s", "peak": alu,
+                         "frac": ach / alu, "flop_per_launch": units[name], "launches": len(ts),
+                         "peak_note": "148 SM x 128 FP32 lanes x 2 x 1965 MHz; 20 flop/interaction"}
+        else:
+            out[name] = {"ms": ms, "launches": len(ts)}
+    return out
+
+
+# ------------------------------------------------------------ CPU oracle baseline
+def cpu_oracle_sample(scale=1.0):
+    """Time the oracle (as it stands) on a bounded sample of one suite graph;
+    return (extrapolated seconds per full graph, description, threads)."""
+    import oracle
+    t = {}
+    n = synth.CFG1_N
+    a, b = synth.vadd_inputs(n)
+    t0 = time.perf_counter(); c = oracle.vadd(a, b); oracle.reduce_sum(c); t["cfg1"] = (time.perf_counter() - t0, 1.0)
+    nk = int((1 << 24) * scale)
+    keys = synth.hist_keys(nk)
+    t0 = time.perf_counter(); oracle.histogram(keys, 256); t["cfg2"] = (time.perf_counter() - t0, synth.CFG2_N / nk)
+    nb = int((1 << 22) * scale)
+    u = synth.bs_rand(nb)
+    t0 = time.perf_counter(); oracle.blackscholes(u); t["cfg3"] = (time.perf_counter() - t0, synth.CFG3_N / nb)
+    n4 = synth.CFG4_MNK
+    rows = max(1, int(16 * scale))
+    A, B = synth.sgemm_inputs(rows, n4, n4)
+    t0 = time.perf_counter(); oracle.sgemm_rows(A, B); t["cfg4"] = (time.perf_counter() - t0, n4 / rows)
+    pos, vel = synth.nbody_state(synth.CFG5_N)
+    ntg = max(1, int(256 * scale))
+    tg = np.arange(ntg)
+    p64 = pos.astype(np.float64)
+    t0 = time.perf_counter(); oracle.nbody_accel(p64, tg)
+    t["cfg5"] = (time.perf_counter() - t0, synth.CFG5_N / ntg * synth.CFG5_STEPS)
+    total = sum(x * s for x, s in t.values())
+    desc = (f"oracle on host cores: cfg1 full 2^20; cfg2 {nk} keys; cfg3 {nb} options; cfg4 {rows} rows of "
+            f"8192x8192x8192; cfg5 {ntg} targets x 2^17 sources x 1 step; each scaled linearly to the full graph")
+    return total, desc, oracle.num_threads(), {k: v[0] * v[1] for k, v in t.items()}
+
+
+def run_reference(args):
+    rank, local, world = dist_env()
+    if rank != 0:
+        return 0
+    steps = []
+    for i in range(args.warmup + args.steps):
+        total, desc, cores, parts = cpu_oracle_sample(scale=0.25)
+        if i >= args.warmup:
+            steps.append(total)
+    sec = statistics.mean(steps)
+    v = 1.0 / sec
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seeded)", "impl": "reference",
+            "config": {"workload": WORKLOAD},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------ main arm
+def run_jacc(args):
+    import torch
+    import torch.distributed as dist
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    comm_ptr = 0
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1508_06791_b200.torch_glue import nccl_comm_ptr
+        dist.barrier()
+        comm_ptr = nccl_comm_ptr()
+    import paper_1508_06791_b200 as J
+    from paper_1508_06791_b200 import jacc
+    peaks = _peaks()
+
+    smode = J.JACC_SGEMM_3XTF32 if args.sgemm_mode == "3xtf32" else J.JACC_SGEMM_FFMA
+    suite = Suite(torch, J, jacc, rank, world, comm_ptr, host_mode=False, sgemm_mode=smode)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")   # 256 MiB > 126 MB L2
+    for _ in range(args.warmup):
+        suite.timed_step(flush)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    launches = 0
+    ktimes = {}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            times.append(suite.timed_step(flush))
+            launches += suite.g.stats()["launches"]
+            for k, v in suite.task_times().items():
+                ktimes.setdefault(k, []).extend(v)
+    torch.cuda.synchronize()
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = 1e3 / ms_per_step
+    kernels = kernel_report(ktimes, suite.units, peaks)
+    clocks = clk.summary()
+    stats = suite.g.stats()
+    suite.g.destroy()
+    del suite
+    torch.cuda.empty_cache()
+
+    # ---- e2e: the same graph through the C-ABI with HOST (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        hs = Suite(torch, J, jacc, rank, world, comm_ptr, host_mode=True, sgemm_mode=smode)
+        hs.g.run()                      # warm-up (device copies allocated)
+        if world > 1:
+            dist.barrier()
+        et = []
+        for _ in range(max(2, min(args.steps, 5))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hs.g.run()
+            et.append(time.perf_counter() - t0)
+        st = hs.g.stats()
+        e_ms = statistics.mean(et) * 1e3
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(st["h2d_bytes"]),
+               "d2h_bytes_per_step": int(st["d2h_bytes"]), "ms_per_step": e_ms,
+               "h2d_count": int(st["h2d_count"]), "d2h_count": int(st["d2h_count"])}
+        hs.g.destroy()
+        del hs
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    dominant = max((k for k in kernels if "frac" in kernels[k]),
+                   key=lambda k: kernels[k]["ms"] * kernels[k]["launches"])
+    dk = kernels[dominant]
+    roofline = {"bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"], "unit": dk["unit"],
+                "frac": dk["frac"], "traffic": None, "kernel": dominant,
+                "peak_source": peaks["source"] if dk["bound"] != "alu" else
+                "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md)"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth/, seeded numpy PCG64)",
+            "config": {"workload": WORKLOAD, "l2": "flushed before every timed step (256 MiB device write)",
+                       "parallelism": f"spmd{world}: index/row/target shards, NCCL allreduce/allgather",
+                       "streams": 4, "sgemm_mode": args.sgemm_mode},
+            "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
+            "e2e": e2e, "step_ms": times, "counted_copies_device_resident": {
+                "h2d": int(stats["h2d_count"]), "d2h": int(stats["d2h_count"])}}
+    if not args.no_cpu_baseline and world == 1:
+        total, desc, cores, parts = cpu_oracle_sample()
+        line["cpu_baseline"] = {"value": 1.0 / total, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": desc, "extrapolated_s_per_graph": total, "parts_s": parts}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["jacc", "reference"], default="jacc")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sgemm-mode", choices=["3xtf32", "ffma"], default="3xtf32")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_jacc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+// blackscholes.cu -- Black-Scholes option pricing (§4.2: "an
+// implementation of the Black Scholes option pricing model ... supplied as an
+// example in the APARAPI source code").  Formula = reading R12 (SURVEY
+// §8(c)-B, the APARAPI sample):
+//   u in [0,1) -> S = 10u + 100(1-u), K = 10u + 100(1-u), T = 1u + 10(1-u),
+//                 R = 0.01u + 0.05(1-u), sigma = 0.01u + 0.10(1-u)
+//   d1 = (ln(S/K) + (R + sigma^2/2) T) / (sigma sqrt T),  d2 = d1 - sigma sqrt T
+//   phi(x): t = 1/(1 + 0.2316419|x|),
+//           y = 1 - 0.398942280 e^{-x^2/2} t (c1 + t(c2 + t(c3 + t(c4 + t c5)))),
+//           phi = y if x >= 0 else 1 - y
+//   call = S phi(d1) - K e^{-RT} phi(d2);  put = K e^{-RT} phi(-d2) - S phi(-d1)
+//
+// sm_100a design: a map at 12 HBM bytes per option whose ~60 fp32 ops and
+// MUFU transcendentals put it close to the issue roof as well.  Work saved
+// without changing the formula's value beyond fp32 rounding:
+//   * one MUFU.RSQ gives 1/(sigma sqrt T) = rsqrt(sigma^2 T), and
+//     sigma sqrt T = sigma^2 T * rsqrt(sigma^2 T);
+//   * the tail w(x) = 0.398942280 e^{-x^2/2} t P(t) depends on |x| only, so
+//     phi(d) and phi(-d) share it (phi(x) = x < 0 ? w : 1 - w and
+//     phi(-x) = x > 0 ? w : 1 - w, exactly the branches of the formula);
+//   * both t = 1/q1, 1/q2 come from ONE reciprocal of q1*q2;
+//   * 128-bit loads/stores, 4 options per thread per iteration.
+// Fast-math intrinsics (rsqrt/ex2/lg2/rcp .approx) are admissible: the
+// tolerance (R12) is |g - o| <= 1e-5 (S + K e^{-RT}) per option.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace jacc_k {
+namespace {
+
+__device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float bs_tail(float t, float x) {
+    const float c1 = 0.319381530f, c2 = -0.356563782f, c3 = 1.781477937f, c4 = -1.821255978f,
+                c5 = 1.330274429f;
+    const float p = fmaf(t, fmaf(t, fmaf(t, fmaf(t, c5, c4), c3), c2), c1);
+    // e^{-x^2/2} = 2^{-x^2 log2(e)/2}
+    const float e = ex2_approx(-0.72134752044448170368f * x * x);
+    return 0.398942280f * e * t * p;
+}
+
+__device__ __forceinline__ void bs_price(float S, float K, float T, float R, float V, float &call, float &put) {
+    const float v2t = V * V * T;
+    const float rs = rsqrtf(v2t);                // 1 / (sigma sqrt T)
+    const float sst = v2t * rs;                  // sigma sqrt T
+    const float lnsk = __logf(__fdividef(S, K));
+    const float d1 = fmaf(fmaf(0.5f * V, V, R), T, lnsk) * rs;
+    const float d2 = d1 - sst;
+    const float kexp = K * ex2_approx(-1.44269504088896340736f * R * T);   // K e^{-RT}
+    const float q1 = fmaf(0.2316419f, fabsf(d1), 1.0f);
+    const float q2 = fmaf(0.2316419f, fabsf(d2), 1.0f);
+    const float r = __fdividef(1.0f, q1 * q2);
+    const float w1 = bs_tail(q2 * r, d1);        // t1 = 1/q1
+    const float w2 = bs_tail(q1 * r, d2);        // t2 = 1/q2
+    const float phi_d1 = d1 < 0.f ? w1 : 1.0f - w1;
+    const float phi_d2 = d2 < 0.f ? w2 : 1.0f - w2;
+    const float phi_md1 = d1 > 0.f ? w1 : 1.0f - w1;   // phi(-d1)
+    const float phi_md2 = d2 > 0.f ? w2 : 1.0f - w2;   // phi(-d2)
+    call = S * phi_d1 - kexp * phi_d2;
+    put = kexp * phi_md2 - S * phi_md1;
+}
+
+__device__ __forceinline__ void bs_aparapi(float u, float &call, float &put) {
+    const float S = fmaf(10.0f, u, 100.0f * (1.0f - u));
+    const float K = fmaf(10.0f, u, 100.0f * (1.0f - u));
+    const float T = fmaf(1.0f, u, 10.0f * (1.0f - u));
+    const float R = fmaf(0.01f, u, 0.05f * (1.0f - u));
+    const float V = fmaf(0.01f, u, 0.10f * (1.0f - u));
+    bs_price(S, K, T, R, V, call, put);
+}
+
+__global__ void __launch_bounds__(256) bs_v4_kernel(const float4 *__restrict__ u4, float4 *__restrict__ call4,
+                                                    float4 *__restrict__ put4, int64_t n4,
+                                                    const float *__restrict__ ut, float *__restrict__ ct,
+                                                    float *__restrict__ pt, int tail) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const float4 u = ld_stream(u4 + i);
+        float4 c, p;
+        bs_aparapi(u.x, c.x, p.x);
+        bs_aparapi(u.y, c.y, p.y);
+        bs_aparapi(u.z, c.z, p.z);
+        bs_aparapi(u.w, c.w, p.w);
+        st_stream(call4 + i, c);
+        st_stream(put4 + i, p);
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tail) bs_aparapi(ut[t], ct[t], pt[t]);
+}
+
+__global__ void __launch_bounds__(256) bs_scalar_kernel(const float *__restrict__ u, float *__restrict__ call,
+                                                        float *__restrict__ put, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        bs_aparapi(u[i], call[i], put[i]);
+}
+
+__global__ void __launch_bounds__(256) bs_soa_kernel(const float *__restrict__ S, const float *__restrict__ K,
+                                                     const float *__restrict__ T, const float *__restrict__ R,
+                                                     const float *__restrict__ V, float *__restrict__ call,
+                                                     float *__restrict__ put, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        bs_price(S[i], K[i], T[i], R[i], V[i], call[i], put[i]);
+}
+
+}  // namespace
+
+cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n, const jacc_schedule_t *s,
+                             cudaStream_t st, int *launches) {
+    if (n <= 0) return cudaSuccess;
+    int grid, block;
+    if (aligned16(u) && aligned16(call) && aligned16(put)) {
+        const int64_t n4 = n / 4;
+        pick_grid(s, (n4 + 255) / 256, 8, 256, &grid, &block);
+        bs_v4_kernel<<<grid, block, 0, st>>>((const float4 *)u, (float4 *)call, (float4 *)put, n4, u + 4 * n4,
+                                             call + 4 * n4, put + 4 * n4, (int)(n - 4 * n4));
+    } else {
+        pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
+        bs_scalar_kernel<<<grid, block, 0, st>>>(u, call, put, n);
+    }
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t blackscholes_soa_f32(const float *S, const float *K, const float *T, const float *R, const float *V,
+                                 float *call, float *put, int64_t n, const jacc_schedule_t *s, cudaStream_t st,
+                                 int *launches) {
+    if (n <= 0) return cudaSuccess;
+    int grid, block;
+    pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
+    bs_soa_kernel<<<grid, block, 0, st>>>(S, K, T, R, V, call, put, n);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace jacc_k

@@ -1,0 +1,47 @@
+// kernels.h -- internal launchers of the sm_100a kernels (not part of the ABI).
+// Each launcher validates nothing the runtime already validated, launches on
+// `st`, adds the number of CUDA kernels it launched to *launches and returns
+// the launch status.  Every kernel is grid-stride or tiled, so the advisory
+// schedule (reading R15) never changes a result.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "jacc.h"
+
+namespace jacc_k {
+
+int sm_count();   // SMs of the current device (148 on B200), cached per device
+
+// c = a + b
+cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,
+                     const jacc_schedule_t *s, cudaStream_t st, int *launches);
+
+// out[0] += sum(x) (out pre-zeroed by the runtime for W)
+size_t reduce_ws_bytes(int64_t n);
+cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws,
+                           const jacc_schedule_t *s, cudaStream_t st, int *launches);
+
+// bins[k] += #{keys == k}
+size_t histogram_ws_bytes(int64_t n, int nbins);
+cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbins, void *ws,
+                          const jacc_schedule_t *s, cudaStream_t st, int *launches);
+
+// APARAPI Black-Scholes
+cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,
+                             const jacc_schedule_t *s, cudaStream_t st, int *launches);
+cudaError_t blackscholes_soa_f32(const float *S, const float *K, const float *T, const float *R,
+                                 const float *V, float *call, float *put, int64_t n,
+                                 const jacc_schedule_t *s, cudaStream_t st, int *launches);
+
+// C = A.B
+size_t sgemm_ws_bytes(const jacc_sgemm_params_t *p);
+cudaError_t sgemm_f32(const float *A, const float *B, float *C, const jacc_sgemm_params_t *p,
+                      void *ws, cudaStream_t st, int *launches);
+
+// north_star N-body step
+cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, float4 *pos_out,
+                           int64_t n_tgt, const jacc_nbody_params_t *p,
+                           const jacc_schedule_t *s, cudaStream_t st, int *launches);
+
+}  // namespace jacc_k

@@ -1,0 +1,98 @@
+// reduce.cu -- Reduction (§2.1.2; §4.2):
+// out[0] += sum_i x[i].
+//
+// The paper's Jacc kernel assigns every partial to an @Atomic(op=ADD) field,
+// "effectively turning the assignment into: result += sum", auto-
+// zeroed (the runtime's MEMSET0 action), and reduces atomic
+// contention by launching fewer threads.  On sm_100a the same
+// result is reached without float atomics (reading R14):
+//   1. 128-bit streaming loads, 4 independent fp32 accumulators per thread;
+//   2. warp shuffle-xor tree, then a block tree through shared memory;
+//   3. SINGLE-PASS cross-block finish: each block stores its partial, bumps
+//      an atomic ticket; the last block to arrive sums the partials in block
+//      order and adds the total to out[0], then re-arms the ticket.
+// For a given n the grid is fixed, so the result is bitwise reproducible.
+// HBM-bound: 4 algorithmic bytes per element.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace jacc_k {
+namespace {
+
+constexpr int kBlock = 512;
+constexpr int kPerSm = 4;           // 4 x 512 threads = 2048 resident per SM
+constexpr int kMaxGrid = 148 * 8;   // workspace sized for any B200 grid
+
+__device__ __forceinline__ float block_sum(float v, float *sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    v = (threadIdx.x < (blockDim.x >> 5)) ? sh[lane] : 0.f;
+    if (warp == 0) v = warp_sum(v);
+    return v;   // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, int64_t n, int64_t head,
+                                                        float *__restrict__ out, float *__restrict__ partials,
+                                                        unsigned *__restrict__ ticket) {
+    __shared__ float sh[32];
+    __shared__ bool last;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    // unaligned head (< 4 scalars), then 128-bit body, then tail (< 4 scalars)
+    if (tid < head) a0 += x[tid];
+    const float4 *x4 = (const float4 *)(x + head);
+    const int64_t n4 = (n - head) / 4;
+    int64_t i = tid;
+    for (; i + stride < n4; i += 2 * stride) {
+        float4 u = ld_stream(x4 + i), v = ld_stream(x4 + i + stride);
+        a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
+        a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+    }
+    if (i < n4) {
+        float4 u = ld_stream(x4 + i);
+        a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
+    }
+    const int64_t t0 = head + 4 * n4;
+    if (tid < n - t0) a1 += x[t0 + tid];
+    float s = block_sum((a0 + a1) + (a2 + a3), sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = s;
+        __threadfence();
+        last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    float p = 0.f;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) p += __ldcg(partials + b);
+    p = block_sum(p, sh);
+    if (threadIdx.x == 0) {
+        out[0] += p;       // @Atomic ADD semantics: result += sum
+        *ticket = 0u;      // re-arm for the next launch (stream-ordered)
+    }
+}
+
+}  // namespace
+
+size_t reduce_ws_bytes(int64_t) { return sizeof(float) * kMaxGrid + 128; }
+
+cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, const jacc_schedule_t *s,
+                           cudaStream_t st, int *launches) {
+    int grid, block;
+    const int64_t head = (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4) < n
+                             ? (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4)
+                             : n;
+    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, &grid, &block);
+    block = kBlock;   // the block tree assumes kBlock threads
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    float *partials = (float *)ws;
+    unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
+    reduce_kernel<<<grid, block, 0, st>>>(x, n, head, out, partials, ticket);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace jacc_k

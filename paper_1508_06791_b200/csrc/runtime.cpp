@@ -1,0 +1,869 @@
+// runtime.cpp -- the Jacc task-graph runtime behind include/jacc.h.
+//
+// PAPER.md §2 / §2.3 and §3.2.1:
+//   task graph (DAG) -> dependency inference -> lowering into
+//   transfers / kernels / collectives -> elimination of
+//   redundant transfers + out-of-order issue of independent kernels (P:61,
+//   P:95) -> traversal-based issue -> sync / commit (P:169-171,
+//   P:214), with per-device persistent state (reading R5).
+//
+// The planner is pure C++ (no CUDA call) so graphs can be built, planned and
+// dumped on a machine without a GPU; the issuer uses the CUDA runtime, the
+// sm_100a kernels (kernels.h) and NCCL resolved at run time (nccl_dl.cpp).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "jacc.h"
+#include "kernels.h"
+#include "nccl_dl.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = std::string(jacc_status_string(status)) + ": " + buf;
+    return status;
+}
+
+size_t dtype_size(int dt) {
+    switch (dt) {
+        case JACC_F32: return 4;
+        case JACC_I32: return 4;
+        case JACC_F32X4: return 16;
+        default: return 0;
+    }
+}
+
+const char *op_name(int op) {
+    switch (op) {
+        case JACC_OP_VADD_F32: return "vadd";
+        case JACC_OP_REDUCE_SUM_F32: return "reduce";
+        case JACC_OP_HISTOGRAM_I32: return "hist";
+        case JACC_OP_BLACKSCHOLES_F32: return "bs";
+        case JACC_OP_BLACKSCHOLES_SOA_F32: return "bs_soa";
+        case JACC_OP_SGEMM_F32: return "sgemm";
+        case JACC_OP_NBODY_STEP_F32: return "nbody";
+        case JACC_OP_ALLREDUCE_SUM: return "allreduce";
+        case JACC_OP_ALLGATHER: return "allgather";
+        case JACC_OP_BROADCAST: return "broadcast";
+        default: return "?";
+    }
+}
+
+bool is_collective(int op) {
+    return op == JACC_OP_ALLREDUCE_SUM || op == JACC_OP_ALLGATHER || op == JACC_OP_BROADCAST;
+}
+
+// index of the @Atomic(op=ADD) output of an op (auto-zeroed in W mode), or -1
+int atomic_out(int op) {
+    return (op == JACC_OP_REDUCE_SUM_F32 || op == JACC_OP_HISTOGRAM_I32) ? 1 : -1;
+}
+
+enum { ST_BUILDING = 0, ST_EXECUTING = 1, ST_DONE = 2, ST_FAILED = 3 };
+
+struct Buffer {
+    uintptr_t host = 0;     // host range start (or the device pointer for DEVICE)
+    size_t bytes = 0;
+    bool device = false;    // JACC_ARG_DEVICE: caller-owned device memory
+    bool cachable = false;  // JACC_ARG_CACHABLE on any use
+    void *dptr = nullptr;   // graph-owned device copy (or == host for DEVICE)
+    bool dev_current = false;  // device copy == host value at the end of the last execute
+    bool invalidated = false;
+    cudaEvent_t ev_h2d = nullptr;
+};
+
+struct TaskArg {
+    int buf;
+    uint64_t count;
+    int dtype;
+    uint32_t access;
+    uint32_t flags;
+};
+
+struct Task {
+    int op;
+    std::vector<TaskArg> args;
+    std::vector<unsigned char> params;
+    jacc_schedule_t sched;
+    bool has_sched = false;
+    std::vector<int> preds;   // inferred edges p -> this
+    int stream = 0;           // planned stream index (-1 = comm stream)
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    float ms = 0.f;
+};
+
+enum ActKind { A_H2D, A_MEMSET0, A_KERNEL, A_COLLECTIVE, A_D2H };
+struct Action {
+    ActKind kind;
+    int buf;    // H2D / MEMSET0 / D2H
+    int task;   // KERNEL / COLLECTIVE / MEMSET0 (owner task)
+};
+
+}  // namespace
+
+struct jacc_graph {
+    jacc_config_t cfg;
+    int state = ST_BUILDING;
+    std::vector<Buffer> bufs;
+    std::vector<Task> tasks;
+    std::vector<Action> plan;
+    std::vector<int> last_writer;
+    bool planned = false;
+    bool have_times = false;
+    // resources
+    bool res_ready = false;
+    int n_streams = 0;
+    cudaStream_t compute[JACC_MAX_STREAMS] = {};
+    bool own_compute = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comm = nullptr;
+    bool own_h2d = false, own_d2h = false, own_comm = false;
+    jacc_stats_t stats;
+    int pending_error = JACC_OK;
+};
+
+// ---------------------------------------------------------------- helpers
+namespace {
+
+int n_streams_of(const jacc_graph *g) {
+    if (g->cfg.flags & (JACC_GRAPH_NAIVE | JACC_GRAPH_SERIAL)) return 1;
+    return g->cfg.n_compute > 0 ? g->cfg.n_compute : 4;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(JACC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+    } while (0)
+
+void *dev_alloc(jacc_graph *g, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (g->cfg.alloc) return g->cfg.alloc(bytes, g->cfg.device, (void *)g->compute[0], g->cfg.alloc_ctx);
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void dev_free(jacc_graph *g, void *p, size_t bytes) {
+    if (!p) return;
+    if (g->cfg.free) g->cfg.free(p, bytes, g->cfg.device, (void *)g->compute[0], g->cfg.alloc_ctx);
+    else cudaFree(p);
+}
+
+// Validate an op's signature: arg count, access, dtype, counts, params (SURVEY §8b "Ops").
+int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void *params,
+             size_t psz) {
+    auto need = [&](int k) -> int {
+        if (n != k) return fail(JACC_ERR_INVALID_ARG, "%s takes %d args, got %d", op_name(op), k, n);
+        return JACC_OK;
+    };
+    auto acc = [&](int i, uint32_t allowed_mask) -> int {
+        // allowed_mask: bit (1 << access)
+        if (!((1u << a[i].access) & allowed_mask))
+            return fail(JACC_ERR_ACCESS, "%s arg %d: access %u not allowed", op_name(op), i, a[i].access);
+        return JACC_OK;
+    };
+    auto dt = [&](int i, int d) -> int {
+        if (a[i].dtype != d) return fail(JACC_ERR_INVALID_ARG, "%s arg %d: dtype %d, want %d", op_name(op), i, a[i].dtype, d);
+        return JACC_OK;
+    };
+    const uint32_t R = 1u << JACC_READ, W = 1u << JACC_WRITE, RW = 1u << JACC_READWRITE;
+    int s;
+#define T(x) if ((s = (x)) != JACC_OK) return s
+    switch (op) {
+        case JACC_OP_VADD_F32:
+            T(need(3)); T(acc(0, R)); T(acc(1, R)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_F32));
+            if (a[1].count != a[0].count || a[2].count != a[0].count)
+                return fail(JACC_ERR_INVALID_ARG, "vadd: counts differ");
+            break;
+        case JACC_OP_REDUCE_SUM_F32:
+            T(need(2)); T(acc(0, R)); T(acc(1, W | RW)); T(dt(0, JACC_F32)); T(dt(1, JACC_F32));
+            if (a[1].count != 1) return fail(JACC_ERR_INVALID_ARG, "reduce: out must have count 1");
+            break;
+        case JACC_OP_HISTOGRAM_I32: {
+            T(need(2)); T(acc(0, R)); T(acc(1, W | RW)); T(dt(0, JACC_I32)); T(dt(1, JACC_I32));
+            if (!params || psz < sizeof(jacc_hist_params_t)) return fail(JACC_ERR_INVALID_ARG, "hist: params");
+            int nb = ((const jacc_hist_params_t *)params)->nbins;
+            if (nb < 1 || nb > 4096) return fail(JACC_ERR_UNSUPPORTED, "hist: nbins %d not in [1, 4096]", nb);
+            if ((int64_t)a[1].count != nb) return fail(JACC_ERR_INVALID_ARG, "hist: bins count != nbins");
+            break;
+        }
+        case JACC_OP_BLACKSCHOLES_F32:
+            T(need(3)); T(acc(0, R)); T(acc(1, W)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_F32));
+            if (a[1].count != a[0].count || a[2].count != a[0].count)
+                return fail(JACC_ERR_INVALID_ARG, "bs: counts differ");
+            break;
+        case JACC_OP_BLACKSCHOLES_SOA_F32:
+            T(need(7));
+            for (int i = 0; i < 5; ++i) T(acc(i, R));
+            T(acc(5, W)); T(acc(6, W));
+            for (int i = 0; i < 7; ++i) {
+                T(dt(i, JACC_F32));
+                if (a[i].count != a[0].count) return fail(JACC_ERR_INVALID_ARG, "bs_soa: counts differ");
+            }
+            break;
+        case JACC_OP_SGEMM_F32: {
+            T(need(3)); T(acc(0, R)); T(acc(1, R)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_F32));
+            if (!params || psz < sizeof(jacc_sgemm_params_t)) return fail(JACC_ERR_INVALID_ARG, "sgemm: params");
+            const jacc_sgemm_params_t *p = (const jacc_sgemm_params_t *)params;
+            if (p->M < 0 || p->N < 0 || p->K < 0 || p->lda < p->K || p->ldb < p->N || p->ldc < p->N)
+                return fail(JACC_ERR_INVALID_ARG, "sgemm: bad shape/strides");
+            if (p->mode != JACC_SGEMM_3XTF32 && p->mode != JACC_SGEMM_FFMA)
+                return fail(JACC_ERR_INVALID_ARG, "sgemm: mode %d", p->mode);
+            auto span = [](int64_t rows, int64_t ld, int64_t cols) -> uint64_t {
+                return rows == 0 || cols == 0 ? 0 : (uint64_t)((rows - 1) * ld + cols);
+            };
+            if (a[0].count < span(p->M, p->lda, p->K) || a[1].count < span(p->K, p->ldb, p->N) ||
+                a[2].count < span(p->M, p->ldc, p->N))
+                return fail(JACC_ERR_INVALID_ARG, "sgemm: buffer smaller than the shape");
+            break;
+        }
+        case JACC_OP_NBODY_STEP_F32: {
+            T(need(3)); T(acc(0, R)); T(acc(1, RW)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_F32X4));
+            if (!params || psz < sizeof(jacc_nbody_params_t)) return fail(JACC_ERR_INVALID_ARG, "nbody: params");
+            const jacc_nbody_params_t *p = (const jacc_nbody_params_t *)params;
+            if (a[2].count != a[1].count) return fail(JACC_ERR_INVALID_ARG, "nbody: vel/pos_out counts differ");
+            if (p->tgt_offset < 0 || (uint64_t)p->tgt_offset + a[1].count > a[0].count)
+                return fail(JACC_ERR_INVALID_ARG, "nbody: targets outside pos_src");
+            if (!(p->eps2 > 0.f)) return fail(JACC_ERR_INVALID_ARG, "nbody: eps2 must be > 0");
+            break;
+        }
+        case JACC_OP_ALLREDUCE_SUM:
+            T(need(1)); T(acc(0, RW));
+            if (a[0].dtype != JACC_F32 && a[0].dtype != JACC_I32)
+                return fail(JACC_ERR_INVALID_ARG, "allreduce: dtype must be f32 or i32");
+            break;
+        case JACC_OP_ALLGATHER:
+            T(need(2)); T(acc(0, R)); T(acc(1, W));
+            if (a[1].dtype != a[0].dtype) return fail(JACC_ERR_INVALID_ARG, "allgather: dtypes differ");
+            if (a[1].count != a[0].count * (uint64_t)g->cfg.world)
+                return fail(JACC_ERR_INVALID_ARG, "allgather: recv count != send count * world");
+            break;
+        case JACC_OP_BROADCAST: {
+            T(need(1)); T(acc(0, RW));
+            if (!params || psz < sizeof(jacc_bcast_params_t)) return fail(JACC_ERR_INVALID_ARG, "broadcast: params");
+            int root = ((const jacc_bcast_params_t *)params)->root;
+            if (root < 0 || root >= g->cfg.world) return fail(JACC_ERR_INVALID_ARG, "broadcast: root");
+            break;
+        }
+        default:
+            return fail(JACC_ERR_INVALID_ARG, "unknown op %d", op);
+    }
+#undef T
+    for (int i = 0; i < n; ++i) {
+        if (!a[i].ptr && a[i].count) return fail(JACC_ERR_INVALID_ARG, "arg %d: NULL pointer", i);
+        if (dtype_size(a[i].dtype) == 0) return fail(JACC_ERR_INVALID_ARG, "arg %d: dtype", i);
+        if (a[i].flags & ~(JACC_ARG_DEVICE | JACC_ARG_CACHABLE))
+            return fail(JACC_ERR_INVALID_ARG, "arg %d: unknown flags", i);
+    }
+    return JACC_OK;
+}
+
+// Find or register the buffer of an argument by its exact byte range.
+int resolve_buffer(jacc_graph *g, const jacc_arg_t &a, std::vector<Buffer> &newbufs, int *id) {
+    uintptr_t lo = (uintptr_t)a.ptr;
+    size_t bytes = a.count * dtype_size(a.dtype);
+    bool dev = a.flags & JACC_ARG_DEVICE;
+    auto check = [&](const Buffer &b, int idx) -> int {
+        if (b.host == lo && b.bytes == bytes) {
+            if (b.device != dev) return fail(JACC_ERR_ALIAS, "buffer %p used both as DEVICE and host", a.ptr);
+            *id = idx;
+            return 1;
+        }
+        if (bytes && b.bytes && lo < b.host + b.bytes && b.host < lo + bytes)
+            return fail(JACC_ERR_ALIAS, "range [%p, +%zu) partially overlaps buffer %d", a.ptr, bytes, idx);
+        return 0;
+    };
+    int nb = (int)g->bufs.size();
+    for (int i = 0; i < nb; ++i) {
+        int r = check(g->bufs[i], i);
+        if (r == 1) return JACC_OK;
+        if (r != 0) return r;
+    }
+    for (int i = 0; i < (int)newbufs.size(); ++i) {
+        int r = check(newbufs[i], nb + i);
+        if (r == 1) return JACC_OK;
+        if (r != 0) return r;
+    }
+    Buffer b;
+    b.host = lo;
+    b.bytes = bytes;
+    b.device = dev;
+    if (dev) b.dptr = a.ptr;
+    newbufs.push_back(b);
+    *id = nb + (int)newbufs.size() - 1;
+    return JACC_OK;
+}
+
+// ------------------------------------------------------------- planner
+// Transfer model G.3 (reading R3) -- identical to the
+// oracle's oracle/graph_model.py:plan, which tests/ compare against.
+void make_plan(jacc_graph *g) {
+    const bool naive = g->cfg.flags & JACC_GRAPH_NAIVE;
+    const int nb = (int)g->bufs.size();
+    std::vector<char> dev_valid(nb), host_valid(nb, 1);
+    g->last_writer.assign(nb, -1);
+    for (int b = 0; b < nb; ++b) {
+        const Buffer &B = g->bufs[b];
+        dev_valid[b] = (B.cachable && B.dev_current && !B.invalidated && B.dptr) ? 1 : 0;
+    }
+    g->plan.clear();
+    // streams: chains stay on the stream of their latest predecessor,
+    // independent tasks go round-robin (out-of-order issue, R6)
+    const int ns = n_streams_of(g);
+    int rr = 0;
+    for (int t = 0; t < (int)g->tasks.size(); ++t) {
+        Task &T = g->tasks[t];
+        if (naive || (g->cfg.flags & JACC_GRAPH_SERIAL)) {
+            T.stream = 0;
+        } else if (is_collective(T.op)) {
+            T.stream = -1;
+        } else {
+            int s = -2;
+            for (int p = (int)T.preds.size() - 1; p >= 0; --p) {
+                int ps = g->tasks[T.preds[p]].stream;
+                if (ps >= 0) { s = ps; break; }
+            }
+            if (s < 0) { s = rr % ns; rr++; }
+            T.stream = s;
+        }
+        const int at = atomic_out(T.op);
+        for (const TaskArg &a : T.args) {
+            if (g->bufs[a.buf].device) continue;
+            if ((a.access & JACC_READ) && (naive || !dev_valid[a.buf])) {
+                g->plan.push_back({A_H2D, a.buf, t});
+                dev_valid[a.buf] = 1;
+            }
+        }
+        for (int k = 0; k < (int)T.args.size(); ++k)
+            if (k == at && T.args[k].access == JACC_WRITE) g->plan.push_back({A_MEMSET0, T.args[k].buf, t});
+        g->plan.push_back({is_collective(T.op) ? A_COLLECTIVE : A_KERNEL, -1, t});
+        for (const TaskArg &a : T.args) {
+            if (a.access & JACC_WRITE) {
+                dev_valid[a.buf] = 1;
+                host_valid[a.buf] = 0;
+                g->last_writer[a.buf] = t;
+                if (naive && !g->bufs[a.buf].device) {
+                    g->plan.push_back({A_D2H, a.buf, t});
+                    host_valid[a.buf] = 1;
+                }
+            }
+        }
+    }
+    if (!naive) {
+        std::vector<int> stale;
+        for (int b = 0; b < nb; ++b)
+            if (!host_valid[b] && !g->bufs[b].device) stale.push_back(b);
+        std::stable_sort(stale.begin(), stale.end(), [&](int x, int y) {
+            return g->last_writer[x] < g->last_writer[y];
+        });
+        for (int b : stale) g->plan.push_back({A_D2H, b, g->last_writer[b]});
+    }
+    g->planned = true;
+}
+
+void plan_counts(const jacc_graph *g, jacc_stats_t *s) {
+    s->h2d_count = s->h2d_bytes = s->d2h_count = s->d2h_bytes = 0;
+    s->memsets = s->kernels = s->collectives = 0;
+    for (const Action &a : g->plan) {
+        switch (a.kind) {
+            case A_H2D: s->h2d_count++; s->h2d_bytes += g->bufs[a.buf].bytes; break;
+            case A_D2H: s->d2h_count++; s->d2h_bytes += g->bufs[a.buf].bytes; break;
+            case A_MEMSET0: s->memsets++; break;
+            case A_KERNEL: s->kernels++; break;
+            case A_COLLECTIVE: s->collectives++; break;
+        }
+    }
+}
+
+std::string dump_text(const jacc_graph *g) {
+    std::string out;
+    char line[256];
+    snprintf(line, sizeof line, "graph tasks=%zu buffers=%zu naive=%d\n", g->tasks.size(), g->bufs.size(),
+             (g->cfg.flags & JACC_GRAPH_NAIVE) ? 1 : 0);
+    out += line;
+    for (size_t t = 0; t < g->tasks.size(); ++t) {
+        const Task &T = g->tasks[t];
+        snprintf(line, sizeof line, "task %zu %s stream=%d args=", t, op_name(T.op), T.stream);
+        out += line;
+        for (size_t k = 0; k < T.args.size(); ++k) {
+            const TaskArg &a = T.args[k];
+            const char *m = a.access == JACC_READ ? "R" : a.access == JACC_WRITE ? "W" : "RW";
+            snprintf(line, sizeof line, "%sb%d:%s%s", k ? "," : "", a.buf, m,
+                     g->bufs[a.buf].device ? ":dev" : "");
+            out += line;
+        }
+        out += "\n";
+    }
+    for (size_t t = 0; t < g->tasks.size(); ++t)
+        for (int p : g->tasks[t].preds) {
+            snprintf(line, sizeof line, "edge %d %zu\n", p, t);
+            out += line;
+        }
+    for (const Action &a : g->plan) {
+        switch (a.kind) {
+            case A_H2D: snprintf(line, sizeof line, "action H2D b%d %zu\n", a.buf, g->bufs[a.buf].bytes); break;
+            case A_D2H: snprintf(line, sizeof line, "action D2H b%d %zu\n", a.buf, g->bufs[a.buf].bytes); break;
+            case A_MEMSET0: snprintf(line, sizeof line, "action MEMSET0 b%d\n", a.buf); break;
+            case A_KERNEL: snprintf(line, sizeof line, "action KERNEL t%d %s\n", a.task, op_name(g->tasks[a.task].op)); break;
+            case A_COLLECTIVE: snprintf(line, sizeof line, "action COLLECTIVE t%d %s\n", a.task, op_name(g->tasks[a.task].op)); break;
+        }
+        out += line;
+    }
+    return out;
+}
+
+// ------------------------------------------------------------- resources
+int ensure_resources(jacc_graph *g) {
+    if (g->res_ready) return JACC_OK;
+    CK(cudaSetDevice(g->cfg.device));
+    g->n_streams = n_streams_of(g);
+    if (g->cfg.n_compute > 0) {
+        for (int i = 0; i < g->cfg.n_compute; ++i) g->compute[i] = (cudaStream_t)g->cfg.compute[i];
+        if (g->n_streams > g->cfg.n_compute) g->n_streams = g->cfg.n_compute;
+    } else {
+        for (int i = 0; i < g->n_streams; ++i) CK(cudaStreamCreateWithFlags(&g->compute[i], cudaStreamNonBlocking));
+        g->own_compute = true;
+    }
+    const bool naive = g->cfg.flags & JACC_GRAPH_NAIVE;
+    if (naive) {
+        g->h2d = g->d2h = g->comm = g->compute[0];
+    } else {
+        if (g->cfg.h2d) g->h2d = (cudaStream_t)g->cfg.h2d;
+        else { CK(cudaStreamCreateWithFlags(&g->h2d, cudaStreamNonBlocking)); g->own_h2d = true; }
+        if (g->cfg.d2h) g->d2h = (cudaStream_t)g->cfg.d2h;
+        else { CK(cudaStreamCreateWithFlags(&g->d2h, cudaStreamNonBlocking)); g->own_d2h = true; }
+        if (g->cfg.comm) g->comm = (cudaStream_t)g->cfg.comm;
+        else { CK(cudaStreamCreateWithFlags(&g->comm, cudaStreamNonBlocking)); g->own_comm = true; }
+    }
+    g->res_ready = true;
+    return JACC_OK;
+}
+
+cudaStream_t stream_of(jacc_graph *g, const Task &T) {
+    if (T.stream < 0) return g->comm;
+    return g->compute[T.stream % g->n_streams];
+}
+
+int prepare_memory(jacc_graph *g) {
+    for (Buffer &B : g->bufs) {
+        if (!B.device && !B.dptr) {
+            B.dptr = dev_alloc(g, B.bytes);
+            if (!B.dptr) return fail(JACC_ERR_OOM, "device copy of %zu bytes", B.bytes);
+            B.dev_current = false;
+        }
+        if (!B.ev_h2d) CK(cudaEventCreateWithFlags(&B.ev_h2d, cudaEventDisableTiming));
+    }
+    for (Task &T : g->tasks) {
+        if (!T.ev_start) CK(cudaEventCreate(&T.ev_start));
+        if (!T.ev_end) CK(cudaEventCreate(&T.ev_end));
+        size_t need = 0;
+        const TaskArg *a = T.args.data();
+        switch (T.op) {
+            case JACC_OP_REDUCE_SUM_F32: need = jacc_k::reduce_ws_bytes((int64_t)a[0].count); break;
+            case JACC_OP_HISTOGRAM_I32:
+                need = jacc_k::histogram_ws_bytes((int64_t)a[0].count,
+                                                  ((const jacc_hist_params_t *)T.params.data())->nbins);
+                break;
+            case JACC_OP_SGEMM_F32: need = jacc_k::sgemm_ws_bytes((const jacc_sgemm_params_t *)T.params.data()); break;
+            default: break;
+        }
+        if (need > T.ws_bytes) {
+            dev_free(g, T.ws, T.ws_bytes);
+            T.ws = dev_alloc(g, need);
+            if (!T.ws) return fail(JACC_ERR_OOM, "workspace of %zu bytes", need);
+            T.ws_bytes = need;
+            // workspaces hold self-resetting counters: start zeroed
+            CK(cudaMemsetAsync(T.ws, 0, need, g->compute[0]));
+            CK(cudaStreamSynchronize(g->compute[0]));
+        }
+    }
+    return JACC_OK;
+}
+
+int nccl_dtype(int dt, uint64_t count, uint64_t *n_out) {
+    if (dt == JACC_F32X4) { *n_out = count * 4; return jacc_nccl::kFloat32; }
+    *n_out = count;
+    return dt == JACC_I32 ? jacc_nccl::kInt32 : jacc_nccl::kFloat32;
+}
+
+int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
+    auto P = [&](int i) { return g->bufs[T.args[i].buf].dptr; };
+    const jacc_schedule_t *sched = T.has_sched ? &T.sched : nullptr;
+    const TaskArg *a = T.args.data();
+    cudaError_t e = cudaSuccess;
+    switch (T.op) {
+        case JACC_OP_VADD_F32:
+            e = jacc_k::vadd_f32((const float *)P(0), (const float *)P(1), (float *)P(2), (int64_t)a[0].count,
+                                 sched, st, launches);
+            break;
+        case JACC_OP_REDUCE_SUM_F32:
+            e = jacc_k::reduce_sum_f32((const float *)P(0), (int64_t)a[0].count, (float *)P(1), T.ws, sched, st,
+                                       launches);
+            break;
+        case JACC_OP_HISTOGRAM_I32:
+            e = jacc_k::histogram_i32((const int32_t *)P(0), (int64_t)a[0].count, (int32_t *)P(1),
+                                      ((const jacc_hist_params_t *)T.params.data())->nbins, T.ws, sched, st,
+                                      launches);
+            break;
+        case JACC_OP_BLACKSCHOLES_F32:
+            e = jacc_k::blackscholes_f32((const float *)P(0), (float *)P(1), (float *)P(2), (int64_t)a[0].count,
+                                         sched, st, launches);
+            break;
+        case JACC_OP_BLACKSCHOLES_SOA_F32:
+            e = jacc_k::blackscholes_soa_f32((const float *)P(0), (const float *)P(1), (const float *)P(2),
+                                             (const float *)P(3), (const float *)P(4), (float *)P(5),
+                                             (float *)P(6), (int64_t)a[0].count, sched, st, launches);
+            break;
+        case JACC_OP_SGEMM_F32:
+            e = jacc_k::sgemm_f32((const float *)P(0), (const float *)P(1), (float *)P(2),
+                                  (const jacc_sgemm_params_t *)T.params.data(), T.ws, st, launches);
+            break;
+        case JACC_OP_NBODY_STEP_F32:
+            e = jacc_k::nbody_step_f32((const float4 *)P(0), (int64_t)a[0].count, (float4 *)P(1), (float4 *)P(2),
+                                       (int64_t)a[1].count, (const jacc_nbody_params_t *)T.params.data(), sched,
+                                       st, launches);
+            break;
+        case JACC_OP_ALLREDUCE_SUM:
+        case JACC_OP_ALLGATHER:
+        case JACC_OP_BROADCAST: {
+            uint64_t n;
+            int dt = nccl_dtype(a[0].dtype, a[0].count, &n);
+            if (g->cfg.world == 1 && !g->cfg.nccl_comm) {
+                if (T.op == JACC_OP_ALLGATHER && a[0].count)
+                    e = cudaMemcpyAsync(P(1), P(0), a[0].count * dtype_size(a[0].dtype), cudaMemcpyDeviceToDevice,
+                                        st);
+                break;
+            }
+            int r;
+            if (T.op == JACC_OP_ALLREDUCE_SUM)
+                r = jacc_nccl::allreduce_sum(P(0), P(0), n, dt, g->cfg.nccl_comm, st);
+            else if (T.op == JACC_OP_ALLGATHER)
+                r = jacc_nccl::allgather(P(0), P(1), n, dt, g->cfg.nccl_comm, st);
+            else
+                r = jacc_nccl::broadcast(P(0), P(0), n, dt, ((const jacc_bcast_params_t *)T.params.data())->root,
+                                         g->cfg.nccl_comm, st);
+            if (r != 0) return fail(JACC_ERR_NCCL, "%s: %s", op_name(T.op), jacc_nccl::last_error());
+            break;
+        }
+        default:
+            return fail(JACC_ERR_INVALID_ARG, "op %d", T.op);
+    }
+    if (e != cudaSuccess) return fail(JACC_ERR_CUDA, "launch %s: %s", op_name(T.op), cudaGetErrorString(e));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(JACC_ERR_CUDA, "launch %s: %s", op_name(T.op), cudaGetErrorString(e));
+    return JACC_OK;
+}
+
+int issue(jacc_graph *g) {
+    const int nb = (int)g->bufs.size();
+    std::vector<char> h2d_issued(nb, 0);
+    std::vector<char> task_done(g->tasks.size(), 0);
+    int launches = 0;
+    jacc_stats_t &S = g->stats;
+    for (size_t ai = 0; ai < g->plan.size(); ++ai) {
+        const Action &A = g->plan[ai];
+        if (A.kind == A_H2D) {
+            Buffer &B = g->bufs[A.buf];
+            CK(cudaMemcpyAsync(B.dptr, (const void *)B.host, B.bytes, cudaMemcpyHostToDevice, g->h2d));
+            CK(cudaEventRecord(B.ev_h2d, g->h2d));
+            h2d_issued[A.buf] = 1;
+        } else if (A.kind == A_KERNEL || A.kind == A_COLLECTIVE) {
+            Task &T = g->tasks[A.task];
+            if (g->cfg.fail_task > 0 && A.task == g->cfg.fail_task - 1)
+                return fail(JACC_ERR_INJECTED, "failure injected at task %d", A.task);
+            cudaStream_t st = stream_of(g, T);
+            for (const TaskArg &a : T.args)
+                if (h2d_issued[a.buf] && g->h2d != st) CK(cudaStreamWaitEvent(st, g->bufs[a.buf].ev_h2d, 0));
+            for (int p : T.preds) {
+                const Task &Pt = g->tasks[p];
+                if (stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_end, 0));
+            }
+            CK(cudaEventRecord(T.ev_start, st));
+            // MEMSET0 actions of this task (auto-zero of @Atomic outputs)
+            for (size_t bj = ai; bj-- > 0;) {
+                const Action &M = g->plan[bj];
+                if (M.kind != A_MEMSET0) break;
+                if (M.task == A.task)
+                    CK(cudaMemsetAsync(g->bufs[M.buf].dptr, 0, g->bufs[M.buf].bytes, st));
+            }
+            int rc = launch_task(g, T, st, &launches);
+            if (rc != JACC_OK) return rc;
+            CK(cudaEventRecord(T.ev_end, st));
+            task_done[A.task] = 1;
+        } else if (A.kind == A_D2H) {
+            Buffer &B = g->bufs[A.buf];
+            const Task &W = g->tasks[A.task];
+            cudaStream_t ws = stream_of(g, W);
+            if (ws != g->d2h) CK(cudaStreamWaitEvent(g->d2h, W.ev_end, 0));
+            CK(cudaMemcpyAsync((void *)B.host, B.dptr, B.bytes, cudaMemcpyDeviceToHost, g->d2h));
+        }
+        // A_MEMSET0 is issued with its task's kernel (same stream)
+    }
+    S.launches = (uint64_t)launches;
+    return JACC_OK;
+}
+
+int sync_all(jacc_graph *g) {
+    cudaError_t first = cudaSuccess;
+    auto chk = [&](cudaError_t e) { if (e != cudaSuccess && first == cudaSuccess) first = e; };
+    for (int i = 0; i < g->n_streams; ++i) chk(cudaStreamSynchronize(g->compute[i]));
+    if (g->h2d) chk(cudaStreamSynchronize(g->h2d));
+    if (g->comm) chk(cudaStreamSynchronize(g->comm));
+    if (g->d2h) chk(cudaStreamSynchronize(g->d2h));
+    if (first != cudaSuccess) return cuda_fail(first, "sync");
+    return JACC_OK;
+}
+
+}  // namespace
+
+// ================================================================ ABI
+extern "C" {
+
+const char *jacc_status_string(int s) {
+    switch (s) {
+        case JACC_OK: return "JACC_OK";
+        case JACC_ERR_INVALID_ARG: return "JACC_ERR_INVALID_ARG";
+        case JACC_ERR_STATE: return "JACC_ERR_STATE";
+        case JACC_ERR_ACCESS: return "JACC_ERR_ACCESS";
+        case JACC_ERR_ALIAS: return "JACC_ERR_ALIAS";
+        case JACC_ERR_DEVICE: return "JACC_ERR_DEVICE";
+        case JACC_ERR_OOM: return "JACC_ERR_OOM";
+        case JACC_ERR_CUDA: return "JACC_ERR_CUDA";
+        case JACC_ERR_NCCL: return "JACC_ERR_NCCL";
+        case JACC_ERR_NOT_FOUND: return "JACC_ERR_NOT_FOUND";
+        case JACC_ERR_UNSUPPORTED: return "JACC_ERR_UNSUPPORTED";
+        case JACC_ERR_INJECTED: return "JACC_ERR_INJECTED";
+        default: return "JACC_ERR_?";
+    }
+}
+
+const char *jacc_last_error(void) { return g_last_error.c_str(); }
+
+int jacc_abi_version(void) { return JACC_ABI_VERSION; }
+
+size_t jacc_abi_sizeof(const char *name) {
+    if (!name) return 0;
+#define S(T) if (!strcmp(name, #T)) return sizeof(T)
+    S(jacc_arg_t); S(jacc_schedule_t); S(jacc_config_t); S(jacc_stats_t);
+    S(jacc_hist_params_t); S(jacc_sgemm_params_t); S(jacc_nbody_params_t); S(jacc_bcast_params_t);
+#undef S
+    return 0;
+}
+
+int jacc_graph_create(jacc_graph_t **out, const jacc_config_t *cfg) {
+    if (!out || !cfg) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+        return fail(JACC_ERR_INVALID_ARG, "rank %d / world %d", cfg->rank, cfg->world);
+    if (cfg->n_compute < 0 || cfg->n_compute > JACC_MAX_STREAMS)
+        return fail(JACC_ERR_INVALID_ARG, "n_compute %d", cfg->n_compute);
+    if (cfg->world > 1 && !cfg->nccl_comm)
+        return fail(JACC_ERR_INVALID_ARG, "world > 1 needs an NCCL communicator");
+    if (cfg->device < 0) return fail(JACC_ERR_INVALID_ARG, "device %d", cfg->device);
+    if ((cfg->alloc == nullptr) != (cfg->free == nullptr))
+        return fail(JACC_ERR_INVALID_ARG, "alloc and free hooks come together");
+    jacc_graph *g = new (std::nothrow) jacc_graph();
+    if (!g) return fail(JACC_ERR_OOM, "host allocation");
+    g->cfg = *cfg;
+    memset(&g->stats, 0, sizeof g->stats);
+    *out = g;
+    return JACC_OK;
+}
+
+int jacc_graph_add_task(jacc_graph_t *g, jacc_op_t op, const jacc_arg_t *args, int nargs, const void *params,
+                        size_t params_size, const jacc_schedule_t *sched, int device, int *task_id) {
+    if (!g || (nargs > 0 && !args) || nargs < 0) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is executing");
+    if (device != g->cfg.device)
+        return fail(JACC_ERR_DEVICE, "task device %d != graph device %d (one process per GPU)", device,
+                    g->cfg.device);
+    int rc = validate(g, op, args, nargs, params, params_size);
+    if (rc != JACC_OK) return rc;
+    Task T;
+    T.op = op;
+    std::vector<Buffer> newbufs;
+    for (int i = 0; i < nargs; ++i) {
+        int id = -1;
+        rc = resolve_buffer(g, args[i], newbufs, &id);
+        if (rc != JACC_OK) return rc;
+        T.args.push_back({id, args[i].count, args[i].dtype, args[i].access, args[i].flags});
+    }
+    // a written buffer may not appear twice in one task (in-place aliasing)
+    for (size_t i = 0; i < T.args.size(); ++i)
+        for (size_t j = 0; j < T.args.size(); ++j)
+            if (i != j && T.args[i].buf == T.args[j].buf && (T.args[i].access & JACC_WRITE))
+                return fail(JACC_ERR_ALIAS, "arg %zu (written) aliases arg %zu", i, j);
+    if (params && params_size) T.params.assign((const unsigned char *)params, (const unsigned char *)params + params_size);
+    if (sched) { T.sched = *sched; T.has_sched = true; }
+    else memset(&T.sched, 0, sizeof T.sched);
+    for (Buffer &b : newbufs) g->bufs.push_back(b);
+    for (const TaskArg &a : T.args)
+        if (a.flags & JACC_ARG_CACHABLE) g->bufs[a.buf].cachable = true;
+    // dependency inference (reading R9)
+    const int t = (int)g->tasks.size();
+    for (int i = 0; i < t; ++i) {
+        bool edge = false;
+        for (const TaskArg &x : g->tasks[i].args)
+            for (const TaskArg &y : T.args)
+                if (x.buf == y.buf && ((x.access & JACC_WRITE) || (y.access & JACC_WRITE))) edge = true;
+        if (edge) T.preds.push_back(i);
+    }
+    g->tasks.push_back(std::move(T));
+    g->planned = false;
+    if (g->state == ST_DONE || g->state == ST_FAILED) g->state = ST_BUILDING;
+    if (task_id) *task_id = t;
+    return JACC_OK;
+}
+
+int jacc_graph_execute(jacc_graph_t *g) {
+    if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
+    if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is already executing");
+    make_plan(g);
+    int rc = ensure_resources(g);
+    if (rc == JACC_OK) rc = prepare_memory(g);
+    if (rc != JACC_OK) { g->state = ST_FAILED; return rc; }
+    plan_counts(g, &g->stats);
+    g->have_times = false;
+    g->state = ST_EXECUTING;
+    rc = issue(g);
+    if (rc != JACC_OK) {
+        sync_all(g);   // drain what was issued; no D2H after the failure point
+        g->state = ST_FAILED;
+        g->pending_error = rc;
+        return rc;
+    }
+    return JACC_OK;
+}
+
+int jacc_graph_sync(jacc_graph_t *g) {
+    if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
+    if (g->state != ST_EXECUTING) {
+        if (g->state == ST_FAILED) return g->pending_error ? g->pending_error : JACC_ERR_STATE;
+        return JACC_OK;
+    }
+    int rc = sync_all(g);
+    if (rc != JACC_OK) {
+        g->state = ST_FAILED;
+        g->pending_error = rc;
+        return rc;
+    }
+    for (Task &T : g->tasks) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, T.ev_start, T.ev_end) == cudaSuccess) T.ms = ms;
+    }
+    g->have_times = true;
+    for (Buffer &B : g->bufs) {
+        if (!B.device) {
+            B.dev_current = true;
+            B.invalidated = false;
+        }
+    }
+    jacc_stats_t &S = g->stats;
+    S.total_h2d_count += S.h2d_count;
+    S.total_h2d_bytes += S.h2d_bytes;
+    S.total_d2h_count += S.d2h_count;
+    S.total_d2h_bytes += S.d2h_bytes;
+    S.total_kernels += S.kernels;
+    S.total_collectives += S.collectives;
+    S.total_launches += S.launches;
+    S.executes += 1;
+    g->state = ST_DONE;
+    g->pending_error = JACC_OK;
+    return JACC_OK;
+}
+
+int jacc_graph_stats(const jacc_graph_t *g, jacc_stats_t *out) {
+    if (!g || !out) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    jacc_graph *gm = const_cast<jacc_graph *>(g);
+    if (gm->state != ST_EXECUTING) {
+        if (!gm->planned) make_plan(gm);
+        if (gm->state == ST_BUILDING) plan_counts(gm, &gm->stats);
+    }
+    *out = g->stats;
+    out->n_tasks = (int32_t)g->tasks.size();
+    out->n_buffers = (int32_t)g->bufs.size();
+    out->state = g->state;
+    return JACC_OK;
+}
+
+int jacc_graph_task_ms(const jacc_graph_t *g, int task_id, float *ms) {
+    if (!g || !ms) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (task_id < 0 || task_id >= (int)g->tasks.size()) return fail(JACC_ERR_NOT_FOUND, "task %d", task_id);
+    if (!g->have_times) return fail(JACC_ERR_STATE, "no completed execute");
+    *ms = g->tasks[task_id].ms;
+    return JACC_OK;
+}
+
+int jacc_graph_dump(jacc_graph_t *g, char *buf, size_t cap, size_t *needed) {
+    if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
+    if (g->state != ST_EXECUTING) make_plan(g);
+    std::string s = dump_text(g);
+    if (needed) *needed = s.size() + 1;
+    if (buf) {
+        if (cap == 0) return fail(JACC_ERR_INVALID_ARG, "cap 0");
+        size_t n = std::min(cap - 1, s.size());
+        memcpy(buf, s.data(), n);
+        buf[n] = 0;
+        if (n < s.size()) return fail(JACC_ERR_INVALID_ARG, "cap %zu < %zu", cap, s.size() + 1);
+    }
+    return JACC_OK;
+}
+
+int jacc_buffer_invalidate(jacc_graph_t *g, const void *host_ptr) {
+    if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
+    if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is executing");
+    for (Buffer &B : g->bufs)
+        if (B.host == (uintptr_t)host_ptr && !B.device) {
+            B.invalidated = true;
+            g->planned = false;
+            return JACC_OK;
+        }
+    return fail(JACC_ERR_NOT_FOUND, "no host buffer at %p", host_ptr);
+}
+
+int jacc_graph_destroy(jacc_graph_t *g) {
+    if (!g) return JACC_OK;
+    if (g->res_ready) {
+        cudaSetDevice(g->cfg.device);
+        sync_all(g);
+        for (Buffer &B : g->bufs) {
+            if (!B.device) dev_free(g, B.dptr, B.bytes);
+            if (B.ev_h2d) cudaEventDestroy(B.ev_h2d);
+        }
+        for (Task &T : g->tasks) {
+            dev_free(g, T.ws, T.ws_bytes);
+            if (T.ev_start) cudaEventDestroy(T.ev_start);
+            if (T.ev_end) cudaEventDestroy(T.ev_end);
+        }
+        if (g->own_compute)
+            for (int i = 0; i < g->n_streams; ++i) cudaStreamDestroy(g->compute[i]);
+        if (g->own_h2d) cudaStreamDestroy(g->h2d);
+        if (g->own_d2h) cudaStreamDestroy(g->d2h);
+        if (g->own_comm) cudaStreamDestroy(g->comm);
+    }
+    delete g;
+    return JACC_OK;
+}
+
+}  // extern "C"

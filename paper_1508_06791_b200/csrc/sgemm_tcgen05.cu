@@ -1,0 +1,347 @@
+// sgemm_tcgen05.cu -- Dense matrix multiply (§4.2, P:484-485, P:525:
+// "SGEMM"), C = A.B, row-major fp32, beta = 0 (reading R13), on the sm_100a
+// 5th-generation tensor cores with the 3xTF32 split (JACC_SGEMM_3XTF32):
+//
+//   x = x_hi + x_lo,  x_hi = x with the low 13 mantissa bits cleared (exactly
+//   representable in TF32), x_lo = x - x_hi (exact in fp32);
+//   A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi     (A_lo.B_lo ~ 2^-22 dropped)
+//
+// accumulated in fp32 in TMEM.  It is used because it meets the north_star
+// tolerance (1e-4 vs the fp64 oracle; DESIGN.md §SGEMM shows 1xTF32 does not
+// on signed inputs).
+//
+// Kernels:
+//   1. split_a: A (M x K, lda) -> A_hi, A_lo  [Mp x Kp], K-major, zero padded;
+//   2. split_bt: B (K x N, ldb) -> B_hi^T, B_lo^T [Np x Kp] (transposed through
+//      shared memory so both UMMA operands are K-major), zero padded;
+//   3. gemm: one 128 x 256 output tile per CTA, warp-specialised --
+//        warp 0     TMA producer: per 32-wide K block, 4 boxes (A_hi, A_lo:
+//                   128x32; B_hi, B_lo: 256x32) into a 2-stage mbarrier ring,
+//                   128B-swizzled;
+//        warp 1     TMEM allocator + single-thread MMA issuer: per K block
+//                   4 k-steps x 3 tcgen05.mma.cta_group::1.kind::tf32
+//                   (M=128, N=256, K=8), D in TMEM (256 fp32 columns);
+//                   tcgen05.commit frees the smem stage / signals the epilogue;
+//        warps 2..5 epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers ->
+//                   global (edge-guarded).
+// Every output element accumulates its K products in the same order for any
+// M/N blocking, so a row block of C computed on one rank equals the same rows
+// computed on one GPU bit for bit.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace jacc_k {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32;      // BK * 4 B = one 128-byte swizzle row
+constexpr int kStages = 2;
+constexpr int kABytes = BM * BK * 4;            // 16 KB
+constexpr int kBBytes = BN * BK * 4;            // 32 KB
+constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;   // 96 KB
+constexpr int kThreads = 192;                   // 6 warps
+constexpr int kTmemCols = 256;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address  [0,14)
+    d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major) [16,30)
+    d |= (uint64_t)(1024 >> 4) << 32;                // SBO = 1024 B   [32,46)
+    d |= (uint64_t)1 << 46;                          // version = 1 (sm_100)
+    d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, M=128, N=256.
+constexpr uint32_t kIdesc = (1u << 4)                // c_format = F32
+                            | (2u << 7)              // a_format = TF32
+                            | (2u << 10)             // b_format = TF32
+                            | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+#define TMEM_LD_32(taddr, r)                                                                                   \
+    asm volatile(                                                                                              \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                     \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),           \
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),           \
+          "=r"(r[30]), "=r"(r[31])                                                                             \
+        : "r"(taddr))
+
+// ------------------------------------------------------------ split kernels
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__global__ void __launch_bounds__(256) split_a_kernel(const float *__restrict__ A, int64_t M, int64_t K, int64_t lda,
+                                                      float *__restrict__ hi, float *__restrict__ lo, int64_t Mp,
+                                                      int64_t Kp) {
+    // grid.x covers Kp in chunks of 1024 (4 per thread), rows stride over grid.y
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (k >= Kp) return;
+    for (int64_t r = blockIdx.y; r < Mp; r += gridDim.y) {
+        float x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = (r < M && k + j < K) ? A[r * lda + k + j] : 0.f;
+        float4 h, l;
+        h.x = tf32_hi(x[0]); h.y = tf32_hi(x[1]); h.z = tf32_hi(x[2]); h.w = tf32_hi(x[3]);
+        l.x = x[0] - h.x; l.y = x[1] - h.y; l.z = x[2] - h.z; l.w = x[3] - h.w;
+        *(float4 *)(hi + r * Kp + k) = h;
+        *(float4 *)(lo + r * Kp + k) = l;
+    }
+}
+
+// B (K x N, row stride ldb) -> hi/lo of B^T, [Np x Kp] row-major (K contiguous).
+__global__ void __launch_bounds__(256) split_bt_kernel(const float *__restrict__ B, int64_t K, int64_t N, int64_t ldb,
+                                                       float *__restrict__ hi, float *__restrict__ lo, int64_t Np,
+                                                       int64_t Kp) {
+    __shared__ float t[32][33];
+    const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t k = k0 + j, n = n0 + tx;
+        t[j][tx] = (k < K && n < N) ? B[k * ldb + n] : 0.f;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t n = n0 + j, k = k0 + tx;
+        if (n < Np && k < Kp) {
+            const float x = t[tx][j];
+            const float h = tf32_hi(x);
+            hi[n * Kp + k] = h;
+            lo[n * Kp + k] = x - h;
+        }
+    }
+}
+
+// ------------------------------------------------------------ GEMM kernel
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                       const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                       float *__restrict__ C, int64_t M, int64_t N, int64_t ldc, int num_kb) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *bars = (uint64_t *)(smem + kStages * kStageBytes);
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 1);
+    const uint32_t full_bar0 = smem_u32(bars), empty_bar0 = smem_u32(bars + kStages),
+                   tmem_full = smem_u32(bars + 2 * kStages);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_blk = blockIdx.y, n_blk = blockIdx.x;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&map_ahi); tma_prefetch(&map_alo); tma_prefetch(&map_bhi); tma_prefetch(&map_blo);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full_bar0 + 8 * s, 1);
+            mbar_init(empty_bar0 + 8 * s, 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- TMA producer
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                mbar_wait(empty_bar0 + 8 * s, ph ^ 1);
+                uint8_t *st = smem + s * kStageBytes;
+                const uint32_t fb = full_bar0 + 8 * s;
+                mbar_expect_tx(fb, kStageBytes);
+                tma_load_2d(smem_u32(st), &map_ahi, kb * BK, m_blk * BM, fb);
+                tma_load_2d(smem_u32(st + kABytes), &map_alo, kb * BK, m_blk * BM, fb);
+                tma_load_2d(smem_u32(st + 2 * kABytes), &map_bhi, kb * BK, n_blk * BN, fb);
+                tma_load_2d(smem_u32(st + 2 * kABytes + kBBytes), &map_blo, kb * BK, n_blk * BN, fb);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---- MMA issuer (one thread for the whole CTA)
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                mbar_wait(full_bar0 + 8 * s, ph);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * kStageBytes);
+                const uint32_t a_hi = base, a_lo = base + kABytes, b_hi = base + 2 * kABytes,
+                               b_lo = base + 2 * kABytes + kBBytes;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {   // K = 8 tf32 = 32 B per MMA
+                    const uint32_t off = k * 32;
+                    mma_tf32(tmem_d, smem_desc(a_hi + off), smem_desc(b_hi + off), (kb | k) != 0);
+                    mma_tf32(tmem_d, smem_desc(a_hi + off), smem_desc(b_lo + off), 1);
+                    mma_tf32(tmem_d, smem_desc(a_lo + off), smem_desc(b_hi + off), 1);
+                }
+                mma_commit(empty_bar0 + 8 * s);   // stage free once these MMAs have read it
+            }
+            mma_commit(tmem_full);                // accumulator complete
+        }
+    } else {   // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31
+        const int q = warp & 3;
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
+        float *crow = C + row * ldc;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem_d + ((uint32_t)(q * 32) << 16) + c * 32;
+            TMEM_LD_32(taddr, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int64_t col0 = (int64_t)n_blk * BN + c * 32;
+            if (row < M) {
+                if (col0 + 32 <= N && ((ldc & 3) == 0) && (((uintptr_t)C & 15) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *(float4 *)(crow + col0 + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                   __uint_as_float(r[j + 2]),
+                                                                   __uint_as_float(r[j + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < N) crow[col0 + j] = __uint_as_float(r[j]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(kTmemCols));
+    }
+}
+
+// ------------------------------------------------------------ host side
+typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn_t get_encode() {
+    static encode_fn_t fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (encode_fn_t)p;
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int box_rows) {
+    encode_fn_t enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
+    cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t sgemm_3xtf32_ws_bytes(const jacc_sgemm_params_t *p) {
+    const int64_t Mp = round_up(p->M > 0 ? p->M : 1, BM), Np = round_up(p->N > 0 ? p->N : 1, BN),
+                  Kp = round_up(p->K > 0 ? p->K : 1, BK);
+    return (size_t)(2 * Mp * Kp + 2 * Np * Kp) * 4 + 4096;
+}
+
+cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sgemm_params_t *p, void *ws,
+                         cudaStream_t st, int *launches) {
+    const int64_t M = p->M, N = p->N, K = p->K;
+    if (M == 0 || N == 0) return cudaSuccess;
+    if (K == 0) {   // C = 0
+        for (int64_t r = 0; r < M; ++r) {
+            cudaError_t e = cudaMemsetAsync(C + r * p->ldc, 0, N * 4, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    const int64_t Mp = round_up(M, BM), Np = round_up(N, BN), Kp = round_up(K, BK);
+    float *ahi = (float *)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
+    float *alo = ahi + Mp * Kp;
+    float *bhi = alo + Mp * Kp;
+    float *blo = bhi + Np * Kp;
+    {
+        dim3 g1((unsigned)((Kp + 1023) / 1024), (unsigned)(Mp < 65535 ? Mp : 65535));
+        split_a_kernel<<<g1, 256, 0, st>>>(A, M, K, p->lda, ahi, alo, Mp, Kp);
+        dim3 g2((unsigned)(Np / 32), (unsigned)(Kp / 32));
+        split_bt_kernel<<<g2, 256, 0, st>>>(B, K, N, p->ldb, bhi, blo, Np, Kp);
+        *launches += 2;
+    }
+    CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
+    if (!make_map(&m_ahi, ahi, Mp, Kp, BM) || !make_map(&m_alo, alo, Mp, Kp, BM) ||
+        !make_map(&m_bhi, bhi, Np, Kp, BN) || !make_map(&m_blo, blo, Np, Kp, BN))
+        return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((unsigned)(Np / BN), (unsigned)(Mp / BM));
+    gemm_3xtf32_kernel<<<grid, kThreads, kSmemBytes, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc,
+                                                           (int)(Kp / BK));
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace jacc_k

@@ -1,0 +1,72 @@
+// vadd.cu -- Vector Addition (§4.2): c[i] = a[i] + b[i].
+//
+// An elementwise map: each element is touched once, so the kernel is pure
+// HBM streaming at 12 algorithmic bytes per element (read a, b; write c).
+// sm_100a design: grid-stride over 128-bit vectors (ld.global.nc.L1::
+// no_allocate / st.global.cs), 4 independent vectors in flight per operand
+// per thread, grid = 8 resident 256-thread blocks on each of the 148 SMs.
+// The iteration space maps onto threads as the @Jacc(ONE_DIMENSION) model
+// says; fewer threads than elements is the block-cyclic mapping
+// of P:163-164 (reading R15): any schedule gives the same bits.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace jacc_k {
+namespace {
+
+constexpr int kUnroll = 4;
+
+__global__ void __launch_bounds__(256) vadd_v4_kernel(const float4 *__restrict__ a, const float4 *__restrict__ b,
+                                                      float4 *__restrict__ c, int64_t n4,
+                                                      const float *__restrict__ at, const float *__restrict__ bt,
+                                                      float *__restrict__ ct, int tail) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n4; i += kUnroll * stride) {
+        float4 x[kUnroll], y[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            x[u] = ld_stream(a + i + u * stride);
+            y[u] = ld_stream(b + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            st_stream(c + i + u * stride, make_float4(x[u].x + y[u].x, x[u].y + y[u].y, x[u].z + y[u].z,
+                                                      x[u].w + y[u].w));
+    }
+    for (; i < n4; i += stride) {
+        float4 x = ld_stream(a + i), y = ld_stream(b + i);
+        st_stream(c + i, make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w));
+    }
+    // the (< 4) trailing scalars
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tail) ct[t] = at[t] + bt[t];
+}
+
+__global__ void __launch_bounds__(256) vadd_scalar_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                                          float *__restrict__ c, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) c[i] = a[i] + b[i];
+}
+
+}  // namespace
+
+cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n, const jacc_schedule_t *s, cudaStream_t st,
+                     int *launches) {
+    if (n <= 0) return cudaSuccess;
+    int grid, block;
+    if (aligned16(a) && aligned16(b) && aligned16(c)) {
+        const int64_t n4 = n / 4;
+        const int tail = (int)(n - 4 * n4);
+        pick_grid(s, (n4 + 255) / 256, 8, 256, &grid, &block);
+        vadd_v4_kernel<<<grid, block, 0, st>>>((const float4 *)a, (const float4 *)b, (float4 *)c, n4, a + 4 * n4,
+                                               b + 4 * n4, c + 4 * n4, tail);
+    } else {
+        pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
+        vadd_scalar_kernel<<<grid, block, 0, st>>>(a, b, c, n);
+    }
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace jacc_k

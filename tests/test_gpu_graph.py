@@ -1,0 +1,175 @@
+"""GPU task-graph semantics through the C-ABI (§2.3, P:286-290;
+SURVEY §8(c)-G): counted copies, elimination soundness (naive == elided
+outputs), serializability against the oracle's serial executor on random
+DAGs, cross-execute residency (CACHABLE, invalidate), failure atomicity and
+out-of-order issue of independent tasks.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import graph_model as gm
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+J = pytest.importorskip("paper_1508_06791_b200")
+from paper_1508_06791_b200 import jacc  # noqa: E402
+from paper_1508_06791_b200.torch_glue import make_graph  # noqa: E402
+
+R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
+
+
+def _graph(**kw):
+    return make_graph(0, **kw)[0]
+
+
+def test_cfg1_counted_copies_and_values():
+    n = synth.CFG1_N
+    a, b = synth.vadd_inputs()
+    c = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R, True), g.a(b, R, True), g.a(c, W)])
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+    g.run()
+    st = g.stats()
+    assert (st["h2d_count"], st["d2h_count"], st["memsets"], st["kernels"]) == (2, 2, 1, 2)
+    assert st["h2d_bytes"] == 8 * n and st["d2h_bytes"] == 4 * n + 4
+    ref_c = oracle.vadd(a, b)
+    assert np.array_equal(c, ref_c)
+    ref, absum = oracle.reduce_sum(ref_c)
+    assert abs(s[0] - ref) <= 1e-4 * absum
+    # 2nd execute: a, b resident (CACHABLE) -> no H2D; same results
+    c[:] = 0; s[:] = 0
+    g.run()
+    st = g.stats()
+    assert (st["h2d_count"], st["d2h_count"]) == (0, 2)
+    assert np.array_equal(c, ref_c)
+    # host writes a -> invalidate -> exactly one H2D again
+    a[:] = 1.0
+    g.invalidate(a)
+    g.run()
+    st = g.stats()
+    assert (st["h2d_count"], st["h2d_bytes"]) == (1, 4 * n)
+    assert np.array_equal(c, oracle.vadd(a, b))
+    g.destroy()
+
+
+def test_naive_equals_elided_and_counts():
+    n = 100003
+    a, b = synth.vadd_inputs(n, seed=3)
+    outs = {}
+    for naive in (True, False):
+        c = np.zeros(n, np.float32); d = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
+        g = _graph(flags=J.JACC_GRAPH_NAIVE if naive else 0)
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(c, R), g.a(b, R), g.a(d, W)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(d, R), g.a(s, W)])
+        g.run()
+        st = g.stats()
+        outs[naive] = (c.copy(), d.copy(), s.copy(), st["h2d_bytes"] + st["d2h_bytes"])
+        g.destroy()
+    for x, y in zip(outs[True][:3], outs[False][:3]):
+        assert np.array_equal(x, y)
+    assert outs[False][3] < outs[True][3]   # optimized bytes strictly smaller
+
+
+def _kernels_for_serial():
+    def vadd(t, arr):
+        arr[2][...] = oracle.vadd(arr[0], arr[1])
+
+    def reduce(t, arr):
+        s, _ = oracle.reduce_sum(arr[0], init=float(arr[1][0]))
+        arr[1][0] = np.float32(s)
+
+    def hist(t, arr):
+        arr[1][...] = oracle.histogram(arr[0], arr[1].size, init=arr[1])
+
+    def allreduce(t, arr):   # world == 1: identity
+        pass
+
+    def allgather(t, arr):
+        arr[1][...] = arr[0]
+    return {"vadd": vadd, "reduce": reduce, "hist": hist, "allreduce": allreduce, "allgather": allgather}
+
+
+def test_serializability_random_dags():
+    """50 random DAGs (3-8 tasks, random R/W modes) executed optimized and
+    out of order == one-by-one insertion-order execution."""
+    from test_abi_cpu import _Pool, _add, _random_tasks
+    rng = np.random.default_rng(2024)
+    kernels = _kernels_for_serial()
+    done = 0
+    while done < 50:
+        tasks = _random_tasks(rng, int(rng.integers(3, 9)))
+        if len(tasks) < 3:
+            continue
+        pool = _Pool(n=4099)
+        allbufs = {**pool.f, **pool.s, **pool.k, **pool.h}
+        for k, v in pool.f.items():
+            v[:] = synth.uniform_f32(v.size, rng.integers(1 << 30))
+        pool.k["K"][:] = rng.integers(-2, 18, pool.k["K"].size)
+        for v in (pool.s["s"], pool.s["t"]):
+            v[:] = rng.random()
+        pool.h["H"][:] = rng.integers(0, 5, 16)
+        host0 = {k: v.copy() for k, v in allbufs.items()}
+        ref = gm.serial_execute(tasks, host0, kernels)
+        g = _graph()
+        for t in tasks:
+            _add(g, pool, t)
+        g.run()
+        for k, v in allbufs.items():
+            if v.dtype == np.int32:
+                assert np.array_equal(v, ref[k]), (k, tasks)
+            else:
+                scale = np.maximum(np.abs(ref[k]), 1.0) * (5e-5 if k in "st" else 0)
+                assert np.all(np.abs(v - ref[k]) <= scale + 1e-6 * np.abs(ref[k])), (k, tasks)
+        g.destroy()
+        done += 1
+
+
+def test_failure_leaves_host_untouched():
+    n = 65536
+    a, b = synth.vadd_inputs(n, seed=1)
+    c = np.full(n, 3.0, np.float32); s = np.full(1, 5.0, np.float32)
+    c0, s0 = c.copy(), s.copy()
+    g = _graph(fail_task=2)   # issuing task 1 fails
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+    with pytest.raises(J.JaccError) as e:
+        g.run()
+    assert e.value.status == J.JACC_ERR_INJECTED
+    assert g.stats()["state"] == 3   # FAILED
+    assert np.array_equal(c, c0) and np.array_equal(s, s0)
+    g.destroy()
+
+
+def test_out_of_order_issue():
+    """a task on DEVICE inputs does not wait for an unrelated
+    task's large H2D: t1 (device inputs) completes before t0's inputs land."""
+    big = 1 << 26   # 256 MiB per input
+    a = torch.empty(big, dtype=torch.float32).pin_memory().uniform_()
+    b = torch.empty(big, dtype=torch.float32).pin_memory().uniform_()
+    c = torch.empty(big, dtype=torch.float32).pin_memory()
+    x = torch.rand(1 << 20, device="cuda"); y = torch.rand(1 << 20, device="cuda")
+    z = torch.empty(1 << 20, device="cuda")
+    g, st = make_graph(0)
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(x, R), g.a(y, R), g.a(z, W)])
+    streams = [int(l.split("stream=")[1].split()[0]) for l in g.dump().splitlines() if l.startswith("task")]
+    assert streams[0] != streams[1]
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_start.record(st["h2d"])
+    g.execute()
+    e_t1 = torch.cuda.Event(enable_timing=True)
+    e_t1.record(st["compute"][streams[1]])      # after t1's kernel
+    e_h2d = torch.cuda.Event(enable_timing=True)
+    e_h2d.record(st["h2d"])                     # after both 256 MiB H2D copies
+    g.sync()
+    torch.cuda.synchronize()
+    assert t_start.elapsed_time(e_t1) < t_start.elapsed_time(e_h2d)
+    assert torch.equal(z, x + y)
+    assert torch.equal(c[:4096], (a[:4096] + b[:4096]))
+    g.destroy()

@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path (through the C-ABI, libjacc.so) vs the CPU oracle
+on the same seeded inputs (synth/), element by element.
+
+Tolerances (written here, derived in DESIGN.md §Tolerances from the
+north_star: "bit-exact for integer histograms and indexing, and for floating
+point within max relative error 1e-5 for maps and 1e-4 against an
+fp64-accumulated oracle for reductions, SGEMM and N-body"):
+  vadd       bit-exact (one IEEE fp32 add; stricter than the 1e-5 bar)
+  reduce     |s - o| <= 1e-4 * sum|x|    (== relative error for x >= 0)
+  histogram  bit-exact
+  BS         |g - o| <= 1e-5 * (S + K e^{-RT})  per option (R12)
+  SGEMM      U[0,1): max elementwise rel <= 1e-4; U[-1,1): normwise <= 1e-4
+             and componentwise |C-R| <= 1e-4 (|A||B|); integer inputs exact
+  N-body     after the steps: |dx_i| <= 1e-4 R (R = 1, ball radius),
+             |dv_i| <= 1e-4 mean|v|; one step at full N: |da|/|a| <= 1e-4
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+J = pytest.importorskip("paper_1508_06791_b200")
+from paper_1508_06791_b200 import jacc  # noqa: E402
+from paper_1508_06791_b200.torch_glue import make_graph  # noqa: E402
+
+R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
+
+
+def _graph(**kw):
+    g, _ = make_graph(0, **kw)
+    return g
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+# ------------------------------------------------------------------ vadd
+@pytest.mark.parametrize("n", [1, 3, 31, 4097, 65539, 1 << 20])
+def test_vadd_bit_exact(n):
+    a, b = synth.vadd_inputs(n, seed=synth.SEED_VADD + n)
+    c = np.zeros(n, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+    g.run()
+    assert np.array_equal(c.view(np.uint32), oracle.vadd(a, b).view(np.uint32))
+    g.destroy()
+
+
+@pytest.mark.parametrize("off", [1, 2, 3])
+def test_vadd_unaligned_device_args(off):
+    n = 10007
+    a, b = synth.vadd_inputs(n + off, seed=77)
+    da, db = _dev(a), _dev(b)
+    dc = torch.zeros(n + off, dtype=torch.float32, device="cuda")
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(da[off:], R), g.a(db[off:], R), g.a(dc[off:], W)])
+    g.run()
+    assert np.array_equal(dc[off:].cpu().numpy(), oracle.vadd(a[off:], b[off:]))
+    assert g.stats()["h2d_count"] == 0
+    g.destroy()
+
+
+# ---------------------------------------------------------------- reduce
+@pytest.mark.parametrize("n", [0, 1, 7, 4097, 1 << 20, (1 << 25) + 5])
+def test_reduce_tolerance(n):
+    x = synth.uniform_f32(n, 31 + n)
+    s = np.zeros(1, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, R), g.a(s, W)])
+    g.run()
+    ref, absum = oracle.reduce_sum(x)
+    assert abs(float(s[0]) - ref) <= 1e-4 * absum + 1e-30
+    g.destroy()
+
+
+def test_reduce_pins_and_determinism():
+    g = _graph()
+    ones = np.ones(1 << 24, np.float32)     # all-ones, N <= 2^24: exact from any fp32 tree
+    s = np.zeros(1, np.float32)
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(ones, R), g.a(s, W)])
+    g.run()
+    assert s[0] == float(1 << 24)
+    g.destroy()
+    x = np.arange(1, 1025, dtype=np.float32)   # S:287 -> 524800
+    s = np.zeros(1, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, R), g.a(s, W)])
+    g.run()
+    assert s[0] == 524800.0
+    g.destroy()
+    x = synth.uniform_f32(3 << 20, 5, -1, 1)
+    outs = []
+    for _ in range(3):
+        s = np.zeros(1, np.float32)
+        g = _graph()
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, R), g.a(s, W)])
+        g.run()
+        outs.append(s[0])
+        g.destroy()
+    assert outs[0] == outs[1] == outs[2]
+
+
+def test_reduce_readwrite_accumulates():
+    x = synth.uniform_f32(100003, 9)
+    s = np.array([1000.0], np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, R), g.a(s, RW)])
+    g.run()
+    ref, absum = oracle.reduce_sum(x, init=1000.0)
+    assert abs(float(s[0]) - ref) <= 1e-4 * (absum + 1000.0)
+    assert g.stats()["memsets"] == 0
+    g.destroy()
+
+
+# ------------------------------------------------------------- histogram
+@pytest.mark.parametrize("n,dist,nbins", [
+    (0, "uniform", 256), (1, "uniform", 256), (255, "uniform", 256), (4099, "uniform", 256),
+    ((1 << 20) + 3, "uniform", 256), (1 << 20, "zeros", 256), (1 << 20, "geometric", 256),
+    ((1 << 20) + 1, "with_out_of_range", 256), (100000, "uniform", 100), (50000, "uniform", 1),
+    (200001, "with_out_of_range", 1000), (100000, "uniform", 4096)])
+def test_hist_bit_exact(n, dist, nbins):
+    keys = synth.hist_keys(n, min(nbins, 256) if dist != "with_out_of_range" else nbins, seed=11 + n, dist=dist)
+    if nbins == 4096:
+        keys = synth.rng(3).integers(0, 4096, n, dtype=np.int32)
+    bins = np.full(nbins, 7, np.int32)
+    g = _graph()
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins, W)], jacc.jacc_hist_params_t(nbins))
+    g.run()
+    assert np.array_equal(bins, oracle.histogram(keys, nbins))
+    g.destroy()
+
+
+@pytest.mark.parametrize("off", [1, 2, 3])
+def test_hist_unaligned_and_accumulate(off):
+    n = 300007
+    keys = synth.hist_keys(n + off, 256, seed=4)
+    dk = _dev(keys)
+    init = np.arange(256, dtype=np.int32)
+    bins = init.copy()
+    g = _graph()
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(dk[off:], R), g.a(bins, RW)], jacc.jacc_hist_params_t(256))
+    g.run()
+    assert np.array_equal(bins, oracle.histogram(keys[off:], 256, init=init))
+    g.destroy()
+
+
+def test_hist_full_size_config2():
+    """BASELINE config 2 size (2^28 keys), the launch configuration bench.py times."""
+    keys = synth.hist_keys()
+    dk = _dev(keys)
+    db = torch.zeros(256, dtype=torch.int32, device="cuda")
+    g = _graph()
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(dk, R), g.a(db, W)], jacc.jacc_hist_params_t(256))
+    g.run()
+    assert np.array_equal(db.cpu().numpy(), oracle.histogram(keys, 256))
+    assert int(db.sum()) == keys.size
+    g.destroy()
+
+
+# --------------------------------------------------------- Black-Scholes
+def _bs_gate(call, put, oc, op, scale):
+    assert np.all(np.abs(call - oc) <= 1e-5 * scale)
+    assert np.all(np.abs(put - op) <= 1e-5 * scale)
+
+
+@pytest.mark.parametrize("n", [1, 5, 4097, 1 << 20])
+def test_bs_aparapi(n):
+    u = synth.bs_rand(n, seed=synth.SEED_BS + n)
+    call = np.zeros(n, np.float32); put = np.zeros(n, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(u, R), g.a(call, W), g.a(put, W)])
+    g.run()
+    oc, op = oracle.blackscholes(u)
+    S = 10 * u.astype(np.float64) + 100 * (1 - u.astype(np.float64))
+    T = 1 * u.astype(np.float64) + 10 * (1 - u.astype(np.float64))
+    Rr = 0.01 * u.astype(np.float64) + 0.05 * (1 - u.astype(np.float64))
+    scale = S + S * np.exp(-Rr * T)
+    _bs_gate(call, put, oc, op, scale)
+    # put-call parity C - P = S - K e^{-RT} (exact in real arithmetic)
+    assert np.all(np.abs((call - put) - (S - S * np.exp(-Rr * T))) <= 1e-5 * scale)
+    g.destroy()
+
+
+def test_bs_full_size_config3_sampled():
+    u = synth.bs_rand()
+    du = _dev(u)
+    dc = torch.empty_like(du); dp = torch.empty_like(du)
+    g = _graph()
+    g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(du, R), g.a(dc, W), g.a(dp, W)])
+    g.run()
+    idx = synth.rng(9).integers(0, u.size, 1 << 16)
+    idx = np.concatenate([idx, [0, 1, 2, 3, u.size - 1]])
+    oc, op = oracle.blackscholes(u[idx])
+    uu = u[idx].astype(np.float64)
+    S = 10 * uu + 100 * (1 - uu); T = uu + 10 * (1 - uu); Rr = 0.01 * uu + 0.05 * (1 - uu)
+    _bs_gate(dc.cpu().numpy()[idx], dp.cpu().numpy()[idx], oc, op, S + S * np.exp(-Rr * T))
+    g.destroy()
+
+
+def test_bs_soa_general_params():
+    rng = np.random.default_rng(21)
+    n = 20011
+    S = rng.uniform(5, 200, n).astype(np.float32); K = rng.uniform(5, 200, n).astype(np.float32)
+    T = rng.uniform(0.05, 10, n).astype(np.float32); Rr = rng.uniform(0, 0.1, n).astype(np.float32)
+    V = rng.uniform(0.01, 0.9, n).astype(np.float32)
+    call = np.zeros(n, np.float32); put = np.zeros(n, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_BLACKSCHOLES_SOA_F32, [g.a(S, R), g.a(K, R), g.a(T, R), g.a(Rr, R), g.a(V, R),
+                                                 g.a(call, W), g.a(put, W)])
+    g.run()
+    oc, op = oracle.blackscholes_soa(S, K, T, Rr, V)
+    scale = S.astype(np.float64) + K.astype(np.float64) * np.exp(-Rr.astype(np.float64) * T)
+    _bs_gate(call, put, oc, op, scale)
+    g.destroy()
+
+
+# ------------------------------------------------------------------ SGEMM
+def _sgemm(A, B, mode, device_args=False):
+    M, K = A.shape
+    N = B.shape[1]
+    g = _graph()
+    if device_args:
+        dA, dB = _dev(A), _dev(B)
+        dC = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        args = [g.a(dA, R), g.a(dB, R), g.a(dC, W)]
+    else:
+        C = np.zeros((M, N), np.float32)
+        args = [g.a(A, R), g.a(B, R), g.a(C, W)]
+    g.add_task(J.JACC_OP_SGEMM_F32, args, jacc.jacc_sgemm_params_t(M, N, K, K, N, N, mode, 0))
+    g.run()
+    out = dC.cpu().numpy() if device_args else C
+    g.destroy()
+    return out
+
+
+SG_SHAPES = [(1, 1, 1), (127, 129, 65), (256, 256, 256), (300, 520, 1000), (1024, 768, 2048)]
+
+
+@pytest.mark.parametrize("mode", [J.JACC_SGEMM_FFMA, J.JACC_SGEMM_3XTF32], ids=["ffma", "3xtf32"])
+@pytest.mark.parametrize("shape", SG_SHAPES)
+def test_sgemm_gates(mode, shape):
+    M, N, K = shape
+    A, B = synth.sgemm_inputs(M, N, K, "int", seed=M + N + K)
+    C = _sgemm(A, B, mode)
+    assert np.array_equal(C.astype(np.float64), oracle.sgemm_rows(A, B)), "integer inputs must be exact"
+    A, B = synth.sgemm_inputs(M, N, K, "unit", seed=M * 3 + K)
+    C = _sgemm(A, B, mode).astype(np.float64)
+    Ro = oracle.sgemm_rows(A, B)
+    assert np.max(np.abs(C - Ro) / np.maximum(np.abs(Ro), 1e-30)) <= 1e-4
+    A, B = synth.sgemm_inputs(M, N, K, "signed", seed=M * 5 + N)
+    C = _sgemm(A, B, mode).astype(np.float64)
+    Ro = oracle.sgemm_rows(A, B)
+    assert np.linalg.norm(C - Ro) <= 1e-4 * np.linalg.norm(Ro)
+    AB = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
+    assert np.all(np.abs(C - Ro) <= 1e-4 * AB + 1e-30)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", [J.JACC_SGEMM_3XTF32], ids=["3xtf32"])
+def test_sgemm_full_size_config4_sampled(mode):
+    n = synth.CFG4_MNK
+    for dist in ("unit", "signed"):
+        A, B = synth.sgemm_inputs(n, n, n, dist)
+        C = _sgemm(A, B, mode, device_args=True)
+        rows = np.concatenate([synth.rng(7).integers(0, n, 12), [0, n - 1]])
+        Ro = oracle.sgemm_rows(A, B, rows)
+        Cs = C[rows].astype(np.float64)
+        if dist == "unit":
+            assert np.max(np.abs(Cs - Ro) / np.abs(Ro)) <= 1e-4
+        else:
+            assert np.linalg.norm(Cs - Ro) <= 1e-4 * np.linalg.norm(Ro)
+        # Freivalds on the whole C (property at any size)
+        x = synth.rng(8).standard_normal(n)
+        lhs = C.astype(np.float64) @ x
+        rhs = A.astype(np.float64) @ (B.astype(np.float64) @ x)
+        bound = np.abs(A).astype(np.float64) @ (np.abs(B).astype(np.float64) @ np.abs(x))
+        assert np.all(np.abs(lhs - rhs) <= 1e-4 * bound)
+
+
+# ----------------------------------------------------------------- N-body
+def _nbody_graph(pos, vel, steps, dt=synth.NBODY_DT, eps2=synth.NBODY_EPS2, G=synth.NBODY_G):
+    n = pos.shape[0]
+    P = [pos.copy(), np.zeros_like(pos)]
+    V = vel.copy()
+    g = _graph()
+    for k in range(steps):
+        g.add_task(J.JACC_OP_NBODY_STEP_F32,
+                   [g.a(P[k % 2], R, True, f32x4=True), g.a(V, RW, True, f32x4=True),
+                    g.a(P[(k + 1) % 2], W, True, f32x4=True)],
+                   jacc.jacc_nbody_params_t(0, dt, eps2, G))
+    g.run()
+    st = g.stats()
+    g.destroy()
+    return P[steps % 2], V, st
+
+
+@pytest.mark.parametrize("n,steps", [(1, 1), (7, 3), (1000, 1), (4096, 10)])
+def test_nbody_steps(n, steps):
+    pos, vel = synth.nbody_state(n, seed=100 + n)
+    gp, gv, st = _nbody_graph(pos, vel, steps)
+    op, ov = oracle.nbody_steps(pos, vel, steps)
+    assert np.max(np.abs(gp[:, :3] - op[:, :3])) <= 1e-4 * 1.0
+    vs = max(np.mean(np.linalg.norm(ov[:, :3], axis=1)), 1e-30)
+    assert np.max(np.abs(gv[:, :3] - ov[:, :3])) <= 1e-4 * vs
+    assert np.array_equal(gp[:, 3], pos[:, 3])
+    if steps > 1:   # SURVEY count table: 10 chained steps -> 2 H2D + 3 D2H
+        assert (st["h2d_count"], st["d2h_count"]) == (2, 3)
+
+
+def test_nbody_full_size_one_step_sampled_and_momentum():
+    n = synth.CFG5_N
+    pos, vel = synth.nbody_state(n)
+    dP = [_dev(pos), torch.zeros_like(_dev(pos))]
+    dV = _dev(vel)
+    g = _graph()
+    for k in range(synth.CFG5_STEPS):
+        g.add_task(J.JACC_OP_NBODY_STEP_F32,
+                   [g.a(dP[k % 2], R, f32x4=True), g.a(dV, RW, f32x4=True), g.a(dP[(k + 1) % 2], W, f32x4=True)],
+                   jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+        if k == 0:
+            pass
+    g.run()
+    v10 = dV.cpu().numpy().astype(np.float64)
+    m = pos[:, 3:4].astype(np.float64)
+    P10 = np.sum(m * v10[:, :3], axis=0)
+    assert np.max(np.abs(P10)) <= 1e-5 * np.sum(m * np.abs(v10[:, :3]))   # momentum conserved
+    g.destroy()
+    # one step, sampled bodies: recover a_i from v_1 = a_i dt (v_0 = 0)
+    dV = _dev(vel); out = torch.zeros_like(dV)
+    g = _graph()
+    g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(_dev(pos), R, f32x4=True), g.a(dV, RW, f32x4=True),
+                                           g.a(out, W, f32x4=True)],
+               jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+    g.run()
+    idx = np.concatenate([synth.rng(3).integers(0, n, 64), [0, n - 1]])
+    a_ref = oracle.nbody_accel(pos.astype(np.float64), idx)
+    a_gpu = dV.cpu().numpy()[idx, :3].astype(np.float64) / synth.NBODY_DT
+    rel = np.linalg.norm(a_gpu - a_ref, axis=1) / np.linalg.norm(a_ref, axis=1)
+    assert np.max(rel) <= 1e-4
+    g.destroy()
+
+
+def test_nbody_shard_invariance_bitwise():
+    n, P = 3000, 4
+    pos, vel = synth.nbody_state(n, seed=5)
+    vel[:, :3] = synth.rng(6).standard_normal((n, 3)).astype(np.float32) * 0.1
+    full_v = vel.copy(); full_p = np.zeros_like(pos)
+    g = _graph()
+    g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(pos, R, f32x4=True), g.a(full_v, RW, f32x4=True),
+                                           g.a(full_p, W, f32x4=True)], jacc.jacc_nbody_params_t(0, 0.016, 0.01, 1.0))
+    g.run(); g.destroy()
+    for r in range(P):
+        lo, hi = synth.shard_range(n, r, P)
+        v = vel[lo:hi].copy(); p = np.zeros_like(v)
+        g = _graph()
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(pos, R, f32x4=True), g.a(v, RW, f32x4=True),
+                                               g.a(p, W, f32x4=True)], jacc.jacc_nbody_params_t(lo, 0.016, 0.01, 1.0))
+        g.run(); g.destroy()
+        assert np.array_equal(v, full_v[lo:hi]) and np.array_equal(p, full_p[lo:hi])
