@@ -26,8 +26,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-relaxed-constexpr",
           "-I", INCLUDE, "-I", CSRC]
-# per-file extras (register budget reports for the hot kernels)
-EXTRA = {}
+# per-file extras: Black-Scholes is computed with the approximate MUFU forms
+# (rcp/lg2/ex2/rsqrt .approx.ftz) -- admissible under its scaled tolerance
+# (R12); -use_fast_math also makes the fp32 ops flush denormals,
+# which removes the denormal range fix-ups around every MUFU.
+EXTRA = {"blackscholes.cu": ["-use_fast_math"]}
 
 
 def _sources():

@@ -34,13 +34,16 @@ __device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2
     return y;
 }
 
+// w(x) = 0.398942280 e^{-x^2/2} t (c1 + t(c2 + t(c3 + t(c4 + t c5)))), with the
+// 0.398942280 factor folded into the polynomial coefficients.
 __device__ __forceinline__ float bs_tail(float t, float x) {
-    const float c1 = 0.319381530f, c2 = -0.356563782f, c3 = 1.781477937f, c4 = -1.821255978f,
-                c5 = 1.330274429f;
+    constexpr double k = 0.398942280;
+    constexpr float c1 = (float)(k * 0.319381530), c2 = (float)(k * -0.356563782), c3 = (float)(k * 1.781477937),
+                    c4 = (float)(k * -1.821255978), c5 = (float)(k * 1.330274429);
     const float p = fmaf(t, fmaf(t, fmaf(t, fmaf(t, c5, c4), c3), c2), c1);
     // e^{-x^2/2} = 2^{-x^2 log2(e)/2}
-    const float e = ex2_approx(-0.72134752044448170368f * x * x);
-    return 0.398942280f * e * t * p;
+    const float e = ex2_approx((-0.72134752044448170368f * x) * x);
+    return e * (t * p);
 }
 
 __device__ __forceinline__ void bs_price(float S, float K, float T, float R, float V, float &call, float &put) {
@@ -64,12 +67,13 @@ __device__ __forceinline__ void bs_price(float S, float K, float T, float R, flo
     put = kexp * phi_md2 - S * phi_md1;
 }
 
+// X = X_lo u + X_hi (1 - u) = X_hi + (X_lo - X_hi) u: one FFMA per parameter.
 __device__ __forceinline__ void bs_aparapi(float u, float &call, float &put) {
-    const float S = fmaf(10.0f, u, 100.0f * (1.0f - u));
-    const float K = fmaf(10.0f, u, 100.0f * (1.0f - u));
-    const float T = fmaf(1.0f, u, 10.0f * (1.0f - u));
-    const float R = fmaf(0.01f, u, 0.05f * (1.0f - u));
-    const float V = fmaf(0.01f, u, 0.10f * (1.0f - u));
+    const float S = fmaf(10.0f - 100.0f, u, 100.0f);
+    const float K = fmaf(10.0f - 100.0f, u, 100.0f);
+    const float T = fmaf(1.0f - 10.0f, u, 10.0f);
+    const float R = fmaf(0.01f - 0.05f, u, 0.05f);
+    const float V = fmaf(0.01f - 0.10f, u, 0.10f);
     bs_price(S, K, T, R, V, call, put);
 }
 
@@ -77,16 +81,37 @@ __global__ void __launch_bounds__(256) bs_v4_kernel(const float4 *__restrict__ u
                                                     float4 *__restrict__ put4, int64_t n4,
                                                     const float *__restrict__ ut, float *__restrict__ ct,
                                                     float *__restrict__ pt, int tail) {
+    // kDepth vectors per trip; the next trip's kDepth loads are issued before
+    // this trip's 4 * kDepth options are priced, so every thread always has
+    // kDepth 128-bit loads in flight (the kernel is otherwise latency-bound:
+    // ncu showed long-scoreboard stalls dominating with one load in flight).
+    constexpr int kDepth = 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-        const float4 u = ld_stream(u4 + i);
-        float4 c, p;
-        bs_aparapi(u.x, c.x, p.x);
-        bs_aparapi(u.y, c.y, p.y);
-        bs_aparapi(u.z, c.z, p.z);
-        bs_aparapi(u.w, c.w, p.w);
-        st_stream(call4 + i, c);
-        st_stream(put4 + i, p);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float4 nxt[kDepth];
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d)
+        nxt[d] = i + d * stride < n4 ? ld_stream(u4 + i + d * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; i < n4; i += kDepth * stride) {
+        float4 cur[kDepth];
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            cur[d] = nxt[d];
+            const int64_t j = i + (kDepth + d) * stride;
+            if (j < n4) nxt[d] = ld_stream(u4 + j);
+        }
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            const int64_t j = i + d * stride;
+            if (j >= n4) break;
+            float4 c, p;
+            bs_aparapi(cur[d].x, c.x, p.x);
+            bs_aparapi(cur[d].y, c.y, p.y);
+            bs_aparapi(cur[d].z, c.z, p.z);
+            bs_aparapi(cur[d].w, c.w, p.w);
+            st_stream(call4 + j, c);
+            st_stream(put4 + j, p);
+        }
     }
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < tail) bs_aparapi(ut[t], ct[t], pt[t]);

@@ -33,14 +33,17 @@ constexpr int kBlock = kWarps * 32;
 constexpr int kU = 4;                     // int4 per lane per chunk (16 keys)
 constexpr int kChunk = 32 * kU;           // int4 per warp chunk
 constexpr int kFlushChunks = 15;          // 15 * 16 = 240 keys <= 255 per lane
-constexpr int kSubWords = 64 * 32;        // 256 bins * 32 lanes / 4 per word
+constexpr int kSubWords = 65 * 32;        // 256 bins * 32 lanes / 4 per word + 1 dummy group
 constexpr int kSmemBytes = kWarps * kSubWords * 4 + 256 * 4;
 
-__device__ __forceinline__ void count_key(unsigned *sub_lane, int k, unsigned nbins) {
-    if ((unsigned)k < nbins) {
-        unsigned *w = sub_lane + ((k >> 2) << 5);      // word (k/4)*32 (+lane via sub_lane)
-        *w += 1u << ((k & 3) << 3);
-    }
+// Branch-free: an out-of-range key is clamped to bin `nbins` (<= 256), a bin
+// that is never merged into the output (bin 256 lives in the dummy group 64).
+// Byte address of (bin kk, lane) = (kk/4)*128 + lane*4 + kk%4 = 32 kk - 31 (kk%4)
+// + lane*4; a lane only ever touches bytes of its own words -> bank `lane`.
+__device__ __forceinline__ void count_key(uint8_t *sub_lane_b, int k, unsigned nbins) {
+    const unsigned kk = min((unsigned)k, nbins);
+    uint8_t *p = sub_lane_b + (32u * kk - 31u * (kk & 3u));
+    *p = (uint8_t)(*p + 1);
 }
 
 // Fold the warp's 8-bit sub-histograms into lane l's totals of bins 8l..8l+7.
@@ -74,8 +77,8 @@ __global__ void __launch_bounds__(kBlock) hist256_kernel(const int4 *__restrict_
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned *sub = smem + warp * kSubWords;
     unsigned *blockh = smem + kWarps * kSubWords;
-    unsigned *sub_lane = sub + lane;
-    for (int g = 0; g < 64; ++g) sub[g * 32 + lane] = 0u;
+    uint8_t *sub_lane = (uint8_t *)(sub + lane);
+    for (int g = 0; g < 65; ++g) sub[g * 32 + lane] = 0u;
     if (threadIdx.x < 256) blockh[threadIdx.x] = 0u;
     __syncthreads();
 
@@ -86,10 +89,15 @@ __global__ void __launch_bounds__(kBlock) hist256_kernel(const int4 *__restrict_
     int since_flush = 0;
     int4 cur[kU], nxt[kU];
     auto load = [&](int64_t ch, int4 *dst) {
+        if ((ch + 1) * kChunk <= n4) {   // interior chunk: unconditional 128-bit loads
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t idx = ch * kChunk + u * 32 + lane;
-            dst[u] = (ch < nchunks && idx < n4) ? ld_stream(keys4 + idx) : make_int4(-1, -1, -1, -1);
+            for (int u = 0; u < kU; ++u) dst[u] = ld_stream(keys4 + ch * kChunk + u * 32 + lane);
+        } else {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t idx = ch * kChunk + u * 32 + lane;
+                dst[u] = (ch < nchunks && idx < n4) ? ld_stream(keys4 + idx) : make_int4(-1, -1, -1, -1);
+            }
         }
     };
     if (c < nchunks) load(c, cur);
@@ -167,14 +175,15 @@ cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbi
         // 3 x 66 KB blocks per SM; the edge keys: [0, head) and [tail0, n)
         pick_grid(s, (nchunks + kWarps - 1) / kWarps, 3, kBlock, &grid, &block);
         block = kBlock;
+        int64_t edge_head = head;
         if (head > 0 && tail0 < n) {
-            // both ends unaligned: count the head with the big kernel path
+            // both ends unaligned: count the head with the small generic kernel
             hist_big_kernel<<<1, 256, nbins * 4, st>>>(keys, head, bins, nbins);
             ++*launches;
-            head = 0;
+            edge_head = 0;
         }
-        const int32_t *edge = head > 0 ? keys : keys + tail0;
-        const int n_edge = (int)(head > 0 ? head : n - tail0);
+        const int32_t *edge = edge_head > 0 ? keys : keys + tail0;
+        const int n_edge = (int)(edge_head > 0 ? edge_head : n - tail0);
         hist256_kernel<<<grid, block, kSmemBytes, st>>>((const int4 *)(keys + head), n4, edge, n_edge, bins, nbins);
     } else {
         pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);

@@ -40,8 +40,9 @@ cudaError_t sgemm_f32(const float *A, const float *B, float *C, const jacc_sgemm
                       void *ws, cudaStream_t st, int *launches);
 
 // north_star N-body step
+size_t nbody_ws_bytes(int64_t n_src, int64_t n_tgt);
 cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, float4 *pos_out,
-                           int64_t n_tgt, const jacc_nbody_params_t *p,
+                           int64_t n_tgt, const jacc_nbody_params_t *p, void *ws,
                            const jacc_schedule_t *s, cudaStream_t st, int *launches);
 
 }  // namespace jacc_k

@@ -5,96 +5,209 @@
 // pos_src holds all n_src bodies (x, y, z, m); targets are bodies
 // tgt_offset .. tgt_offset + n_tgt - 1 (a rank's shard in SPMD, R17).
 //
-// sm_100a design (FP32-pipe bound, 12 fp32 ops + 1 MUFU.RSQ / interaction):
-//   * sources stream through shared memory in tiles of kTile bodies (float4),
-//     every thread keeps kTpt targets in registers, so each LDS.128 of a
-//     source feeds kTpt interactions;
-//   * accumulation is TILE-PARTIAL: each tile's contributions are summed
-//     separately, then added to the running total in tile order (the
-//     accuracy of a blocked sum, SURVEY §8(c)-N [exp]);
-//   * the self term is included: x_j - x_i = 0 and eps2 > 0 make it exactly 0;
-//   * padding sources beyond n_src have m = 0 at the origin (contribute 0).
-// The j order is the global order for every target, so a rank computing a
-// shard gets the same bits as one GPU computing everything (§8(e)).
+// sm_100a design (FP32-pipe bound: 12 fp32 ops + 1 MUFU.RSQ per interaction):
+//   * work unit = (256 targets) x (one chunk of kChunk = 8192 sources); the
+//     chunk size depends on nothing but the source count, so every rank of a
+//     sharded run sums a target's sources in exactly the same groups as one
+//     GPU does (bitwise shard invariance, §8(e)), and 2^17 bodies give 8192
+//     units -- 55 per SM, so the 148 SMs finish within 2% of each other;
+//   * sources stream through shared memory in tiles; each thread holds
+//     kTpt = 4 targets in registers, so one shared-memory load of a source
+//     feeds 4 interactions;
+//   * accumulation is TILE-PARTIAL (each tile summed separately, then added
+//     in tile order), chunk partials go to a workspace and a second kernel
+//     adds the chunks in order and applies kick + drift;
+//   * the x2 variant packs 2 targets per register pair and uses the sm_100
+//     paired FP32 instructions (FADD2 / FFMA2 / FMUL2): half the FP32 issue
+//     slots for the same arithmetic;
+//   * the self term is included: x_j - x_i = 0 with eps2 > 0 contributes 0;
+//     padding sources (j >= n_src) have m = 0 at the origin (contribute 0).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace jacc_k {
 namespace {
 
-constexpr int kBlock = 128;
-constexpr int kTpt = 2;                 // targets per thread
-constexpr int kTile = kBlock;           // sources per shared-memory tile
+constexpr int kBlock = 64;
+constexpr int kTile = 256;                    // sources per shared-memory tile
+constexpr int kChunk = 8192;                  // sources per work unit
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-__global__ void __launch_bounds__(kBlock) nbody_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
-                                                       float4 *__restrict__ vel, float4 *__restrict__ pos_out,
-                                                       int64_t n_tgt, int64_t tgt_offset, float dt, float eps2,
-                                                       float G) {
-    __shared__ float4 tile[kTile];
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * kTpt);
-    float xi[kTpt], yi[kTpt], zi[kTpt];
-    float ax[kTpt], ay[kTpt], az[kTpt];
+// One work unit: kBlock * (2P + S) targets x one chunk of sources.  P target
+// PAIRS use the paired FP32 instructions (FADD2/FFMA2/FMUL2, which run on the
+// FMA-heavy pipe), S further targets use scalar FP32 (which the scheduler can
+// place on the other FP32 pipe): mixing the two keeps both FP32 pipes and the
+// MUFU (rsqrt) busy.  Target k of thread tid is t0 + tid + k * kBlock.
+template <int P, int S>
+__global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
+                                                               int64_t n_tgt, int64_t tgt_offset, float eps2,
+                                                               float4 *__restrict__ part) {
+    constexpr int T = 2 * P + S;
+    __shared__ float4 tile[2 * kTile];   // per source: (x, x, y, y), (z, z, m, m)
+    const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
+    const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
+    const int64_t j_end = min(j_begin + kChunk, n_src);
+    float2 nx[P > 0 ? P : 1], ny[P > 0 ? P : 1], nz[P > 0 ? P : 1];     // -x of target pairs
+    float2 ax[P > 0 ? P : 1], ay[P > 0 ? P : 1], az[P > 0 ? P : 1];
+    float sx[S > 0 ? S : 1], sy[S > 0 ? S : 1], sz[S > 0 ? S : 1];
+    float bx[S > 0 ? S : 1], by[S > 0 ? S : 1], bz[S > 0 ? S : 1];
+    auto load_t = [&](int k) {
+        const int64_t t = t0 + threadIdx.x + k * kBlock;
+        return t < n_tgt ? pos_src[tgt_offset + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
 #pragma unroll
-    for (int k = 0; k < kTpt; ++k) {
-        const int64_t t = base + threadIdx.x + k * kBlock;
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t < n_tgt) p = pos_src[tgt_offset + t];
-        xi[k] = p.x; yi[k] = p.y; zi[k] = p.z;
-        ax[k] = ay[k] = az[k] = 0.f;
+    for (int p = 0; p < P; ++p) {
+        const float4 a = load_t(2 * p), b = load_t(2 * p + 1);
+        nx[p] = f2(-a.x, -b.x); ny[p] = f2(-a.y, -b.y); nz[p] = f2(-a.z, -b.z);
+        ax[p] = ay[p] = az[p] = f2(0.f, 0.f);
     }
-    for (int64_t j0 = 0; j0 < n_src; j0 += kTile) {
-        const int64_t j = j0 + threadIdx.x;
-        tile[threadIdx.x] = j < n_src ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        const float4 a = load_t(2 * P + q);
+        sx[q] = a.x; sy[q] = a.y; sz[q] = a.z;
+        bx[q] = by[q] = bz[q] = 0.f;
+    }
+    const float2 e2 = f2(eps2, eps2);
+    for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
         __syncthreads();
-        float tx[kTpt], ty[kTpt], tz[kTpt];
 #pragma unroll
-        for (int k = 0; k < kTpt; ++k) tx[k] = ty[k] = tz[k] = 0.f;
-#pragma unroll 8
+        for (int q = 0; q < kTile / kBlock; ++q) {
+            const int s = threadIdx.x + q * kBlock;
+            const int64_t j = j0 + s;
+            const float4 v = j < j_end ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            tile[2 * s] = make_float4(v.x, v.x, v.y, v.y);
+            tile[2 * s + 1] = make_float4(v.z, v.z, v.w, v.w);
+        }
+        __syncthreads();
+        float2 tx[P > 0 ? P : 1], ty[P > 0 ? P : 1], tz[P > 0 ? P : 1];
+        float ux[S > 0 ? S : 1], uy[S > 0 ? S : 1], uz[S > 0 ? S : 1];
+#pragma unroll
+        for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = f2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < S; ++q) ux[q] = uy[q] = uz[q] = 0.f;
+#pragma unroll 4
         for (int s = 0; s < kTile; ++s) {
-            const float4 q = tile[s];
+            const float4 A = tile[2 * s], B = tile[2 * s + 1];
+            const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
 #pragma unroll
-            for (int k = 0; k < kTpt; ++k) {
-                const float dx = q.x - xi[k], dy = q.y - yi[k], dz = q.z - zi[k];
+            for (int p = 0; p < P; ++p) {
+                const float2 dx = __fadd2_rn(xj, nx[p]), dy = __fadd2_rn(yj, ny[p]), dz = __fadd2_rn(zj, nz[p]);
+                float2 r2 = __ffma2_rn(dx, dx, e2);
+                r2 = __ffma2_rn(dy, dy, r2);
+                r2 = __ffma2_rn(dz, dz, r2);
+                const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+                const float2 sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
+                tx[p] = __ffma2_rn(dx, sc, tx[p]);
+                ty[p] = __ffma2_rn(dy, sc, ty[p]);
+                tz[p] = __ffma2_rn(dz, sc, tz[p]);
+            }
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+                const float dx = A.x - sx[q], dy = A.z - sy[q], dz = B.x - sz[q];
                 const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
                 const float inv = rsqrt_approx(r2);
-                const float sc = q.w * inv * inv * inv;
-                tx[k] = fmaf(dx, sc, tx[k]);
-                ty[k] = fmaf(dy, sc, ty[k]);
-                tz[k] = fmaf(dz, sc, tz[k]);
+                const float sc = (B.z * inv) * (inv * inv);
+                ux[q] = fmaf(dx, sc, ux[q]);
+                uy[q] = fmaf(dy, sc, uy[q]);
+                uz[q] = fmaf(dz, sc, uz[q]);
             }
         }
 #pragma unroll
-        for (int k = 0; k < kTpt; ++k) { ax[k] += tx[k]; ay[k] += ty[k]; az[k] += tz[k]; }
-        __syncthreads();
+        for (int p = 0; p < P; ++p) {
+            ax[p] = __fadd2_rn(ax[p], tx[p]);
+            ay[p] = __fadd2_rn(ay[p], ty[p]);
+            az[p] = __fadd2_rn(az[p], tz[p]);
+        }
+#pragma unroll
+        for (int q = 0; q < S; ++q) { bx[q] += ux[q]; by[q] += uy[q]; bz[q] += uz[q]; }
+    }
+    float4 *out = part + (int64_t)blockIdx.y * n_tgt;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int64_t ta = t0 + threadIdx.x + (2 * p) * kBlock, tb = ta + kBlock;
+        if (ta < n_tgt) out[ta] = make_float4(ax[p].x, ay[p].x, az[p].x, 0.f);
+        if (tb < n_tgt) out[tb] = make_float4(ax[p].y, ay[p].y, az[p].y, 0.f);
     }
 #pragma unroll
-    for (int k = 0; k < kTpt; ++k) {
-        const int64_t t = base + threadIdx.x + k * kBlock;
-        if (t >= n_tgt) continue;
-        float4 v = vel[t];
-        v.x = fmaf(G * ax[k], dt, v.x);
-        v.y = fmaf(G * ay[k], dt, v.y);
-        v.z = fmaf(G * az[k], dt, v.z);
-        vel[t] = v;
-        const float m = pos_src[tgt_offset + t].w;
-        pos_out[t] = make_float4(fmaf(v.x, dt, xi[k]), fmaf(v.y, dt, yi[k]), fmaf(v.z, dt, zi[k]), m);
+    for (int q = 0; q < S; ++q) {
+        const int64_t t = t0 + threadIdx.x + (2 * P + q) * kBlock;
+        if (t < n_tgt) out[t] = make_float4(bx[q], by[q], bz[q], 0.f);
     }
+}
+
+// ---- chunk sum (in chunk order) + kick + drift ---------------------------
+__global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restrict__ part, int nchunks,
+                                                           const float4 *__restrict__ pos_src, int64_t tgt_offset,
+                                                           float4 *__restrict__ vel, float4 *__restrict__ pos_out,
+                                                           int64_t n_tgt, float dt, float G) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tgt) return;
+    float4 a = part[t];
+    for (int c = 1; c < nchunks; ++c) {
+        const float4 b = part[(int64_t)c * n_tgt + t];
+        a.x += b.x; a.y += b.y; a.z += b.z;
+    }
+    float4 v = vel[t];
+    v.x = fmaf(G * a.x, dt, v.x);
+    v.y = fmaf(G * a.y, dt, v.y);
+    v.z = fmaf(G * a.z, dt, v.z);
+    vel[t] = v;
+    const float4 p = pos_src[tgt_offset + t];
+    pos_out[t] = make_float4(fmaf(v.x, dt, p.x), fmaf(v.y, dt, p.y), fmaf(v.z, dt, p.z), p.w);
+}
+
+typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
+struct Variant { partial_fn fn; int tpt; };
+
+Variant variant() {
+    static Variant v = {nullptr, 0};
+    if (!v.fn) {
+        const char *e = getenv("JACC_NBODY_VARIANT");   // experiments only: "P,S"
+        int P = 2, S = 0;
+        if (e) sscanf(e, "%d,%d", &P, &S);
+#define V(p, s) if (P == p && S == s) v = {nbody_partial_kernel<p, s>, 2 * p + s}
+        V(2, 0); V(0, 4); V(2, 2); V(3, 0); V(4, 0); V(1, 0);
+#undef V
+        if (!v.fn) v = {nbody_partial_kernel<2, 0>, 4};
+    }
+    return v;
 }
 
 }  // namespace
 
+size_t nbody_ws_bytes(int64_t n_src, int64_t n_tgt) {
+    const int64_t nchunks = (n_src + kChunk - 1) / kChunk;
+    return (size_t)(nchunks > 0 ? nchunks : 1) * (size_t)(n_tgt > 0 ? n_tgt : 1) * sizeof(float4);
+}
+
 cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, float4 *pos_out, int64_t n_tgt,
-                           const jacc_nbody_params_t *p, const jacc_schedule_t *, cudaStream_t st, int *launches) {
+                           const jacc_nbody_params_t *p, void *ws, const jacc_schedule_t *, cudaStream_t st,
+                           int *launches) {
     if (n_tgt <= 0) return cudaSuccess;
-    const int64_t grid = (n_tgt + kBlock * kTpt - 1) / (kBlock * kTpt);
-    nbody_kernel<<<(unsigned)grid, kBlock, 0, st>>>(pos_src, n_src, vel, pos_out, n_tgt, p->tgt_offset, p->dt,
-                                                    p->eps2, p->G);
+    float4 *part = (float4 *)ws;
+    const int64_t nchunks = (n_src + kChunk - 1) / kChunk;
+    if (nchunks == 0) {   // no sources: a = 0
+        cudaError_t e = cudaMemsetAsync(part, 0, n_tgt * sizeof(float4), st);
+        if (e != cudaSuccess) return e;
+    } else {
+        const Variant v = variant();
+        const int64_t per_block = (int64_t)kBlock * v.tpt;
+        dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nchunks);
+        v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);
+        ++*launches;
+    }
+    nbody_finish_kernel<<<(unsigned)((n_tgt + 255) / 256), 256, 0, st>>>(part, nchunks > 0 ? (int)nchunks : 1,
+                                                                         pos_src, p->tgt_offset, vel, pos_out, n_tgt,
+                                                                         p->dt, p->G);
     ++*launches;
     return cudaGetLastError();
 }

@@ -1,0 +1,97 @@
+#!/usr/bin/env python
+"""Kernel micro-bench through the C-ABI (device-resident args), for timing a
+single op in isolation and for short ncu captures:
+
+    python scripts/kbench.py hist|bs|vadd|reduce|sgemm|nbody [--n N] [--reps R]
+
+Prints one JSON line per op: mean/min device ms per launch (CUDA events on the
+stream the task runs on = jacc_graph_task_ms) and achieved GB/s or TFLOP/s.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("ops", nargs="+")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--mode", default="3xtf32")
+    a = ap.parse_args()
+    import torch
+    import paper_1508_06791_b200 as J
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph
+    R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    for op in a.ops:
+        g, _ = make_graph(0, n_streams=1)
+        keep = []
+
+        def D(x):
+            t = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+            keep.append(t)
+            return t
+        if op == "vadd":
+            n = a.n or synth.CFG1_N
+            x, y = synth.vadd_inputs(n)
+            g.add_task(J.JACC_OP_VADD_F32, [g.a(D(x), R), g.a(D(y), R), g.a(D(np.zeros(n, np.float32)), W)])
+            units, kind = 12 * n, "GB/s"
+        elif op == "reduce":
+            n = a.n or synth.CFG1_N
+            g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(D(synth.uniform_f32(n, 1)), R),
+                                                   g.a(D(np.zeros(1, np.float32)), W)])
+            units, kind = 4 * n, "GB/s"
+        elif op == "hist":
+            n = a.n or synth.CFG2_N
+            g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(D(synth.hist_keys(n)), R), g.a(D(np.zeros(256, np.int32)), W)],
+                       jacc.jacc_hist_params_t(256))
+            units, kind = 4 * n, "GB/s"
+        elif op == "bs":
+            n = a.n or synth.CFG3_N
+            g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(D(synth.bs_rand(n)), R), g.a(D(np.zeros(n, np.float32)), W),
+                                                     g.a(D(np.zeros(n, np.float32)), W)])
+            units, kind = 12 * n, "GB/s"
+        elif op == "sgemm":
+            n = a.n or synth.CFG4_MNK
+            A, B = synth.sgemm_inputs(n, n, n)
+            mode = J.JACC_SGEMM_3XTF32 if a.mode == "3xtf32" else J.JACC_SGEMM_FFMA
+            g.add_task(J.JACC_OP_SGEMM_F32, [g.a(D(A), R), g.a(D(B), R), g.a(D(np.zeros((n, n), np.float32)), W)],
+                       jacc.jacc_sgemm_params_t(n, n, n, n, n, n, mode, 0))
+            units, kind = 2 * n ** 3, "TFLOP/s"
+        elif op == "nbody":
+            n = a.n or synth.CFG5_N
+            pos, vel = synth.nbody_state(n)
+            g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(D(pos), R, f32x4=True), g.a(D(vel), RW, f32x4=True),
+                                                   g.a(D(np.zeros_like(pos)), W, f32x4=True)],
+                       jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+            units, kind = 20 * n * n, "TFLOP/s"
+        else:
+            raise SystemExit(f"unknown op {op}")
+        ms = []
+        for i in range(a.reps + 2):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            g.run()
+            if i >= 2:
+                ms.append(g.task_ms(0))
+        mean = sum(ms) / len(ms)
+        scale = 1e9 if kind == "GB/s" else 1e12
+        print(json.dumps({"op": op, "n": n, "mean_ms": mean, "min_ms": min(ms),
+                          "achieved": units / (mean * 1e-3) / scale, "best": units / (min(ms) * 1e-3) / scale,
+                          "unit": kind, "launches_per_task": g.stats()["launches"]}), flush=True)
+        g.destroy()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,119 @@
+"""Multi-process (world_size 2, gloo, CPU) checks of the N>1 path's host logic.
+
+The GPU box used here has one GPU, so the SPMD decomposition bench.py uses at
+N>1 is verified on CPU: every rank takes its shard
+(synth.shard_range), computes it with the oracle, and the ranks combine with
+the same collective the GPU path issues through NCCL (allreduce of partial
+sums / bins, allgather of N-body positions).  The combination must equal the
+single-process oracle -- bitwise where §8(e) says so -- and each rank's
+libjacc.so plan (built with world = 2) must have the counted copies of the
+SURVEY count table.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        import synth
+        res = {}
+        # cfg2: histogram shards + allreduce(bins)  -> bitwise
+        keys = synth.hist_keys(1 << 20, seed=7)
+        lo, hi = synth.shard_range(keys.size, rank, world)
+        bins = torch.from_numpy(oracle.histogram(keys[lo:hi], 256).astype(np.int64))
+        dist.all_reduce(bins)
+        res["hist"] = bool(np.array_equal(bins.numpy(), oracle.histogram(keys, 256)))
+        # cfg1: vadd shard -> partial sum -> allreduce  (tolerance 1e-4 sum|x|)
+        a, b = synth.vadd_inputs(1 << 16)
+        lo, hi = synth.shard_range(a.size, rank, world)
+        c = oracle.vadd(a[lo:hi], b[lo:hi])
+        s = torch.tensor([oracle.reduce_sum(c)[0]], dtype=torch.float64)
+        dist.all_reduce(s)
+        ref, absum = oracle.reduce_sum(oracle.vadd(a, b))
+        res["reduce"] = bool(abs(s.item() - ref) <= 1e-12 * absum)
+        # cfg4: SGEMM row blocks (B replicated) + allgather rows -> bitwise
+        A, B = synth.sgemm_inputs(64, 48, 80, "signed")
+        lo, hi = synth.shard_range(64, rank, world)
+        part = torch.from_numpy(oracle.sgemm_rows(A, B, np.arange(lo, hi)))
+        parts = [torch.zeros((synth.shard_range(64, r, world)[1] - synth.shard_range(64, r, world)[0], 48),
+                             dtype=torch.float64) for r in range(world)]
+        dist.all_gather(parts, part)
+        res["sgemm"] = bool(np.array_equal(torch.cat(parts).numpy(), oracle.sgemm_rows(A, B)))
+        # cfg5: N-body target shards, positions all-gathered every step -> bitwise
+        n, steps = 96, 3
+        pos, vel = synth.nbody_state(n, seed=3)
+        lo, hi = synth.shard_range(n, rank, world)
+        P = pos.astype(np.float64).copy()
+        V = vel[lo:hi].astype(np.float64).copy()
+        for _ in range(steps):
+            acc = oracle.nbody_accel(P, np.arange(lo, hi))
+            V[:, :3] += acc * synth.NBODY_DT
+            mine = P[lo:hi].copy()
+            mine[:, :3] += V[:, :3] * synth.NBODY_DT
+            gathered = [torch.zeros((synth.shard_range(n, r, world)[1] - synth.shard_range(n, r, world)[0], 4),
+                                    dtype=torch.float64) for r in range(world)]
+            dist.all_gather(gathered, torch.from_numpy(mine))
+            P = torch.cat(gathered).numpy()
+        fp, fv = oracle.nbody_steps(pos, vel, steps)
+        res["nbody"] = bool(np.array_equal(P, fp) and np.array_equal(V, fv[lo:hi]))
+        # each rank's libjacc plan with world = 2: counted copies per rank
+        import paper_1508_06791_b200 as J
+        from paper_1508_06791_b200 import jacc
+        g = J.Graph(rank=rank, world=world, nccl_comm=0x1)   # plan/dump only: NCCL is never called
+        L = [np.zeros((n // world, 4), np.float32) for _ in range(2)]
+        Vl = np.zeros((n // world, 4), np.float32)
+        ALL = torch.zeros((n, 4), dtype=torch.float32)
+        for k in range(10):
+            g.add_task(J.JACC_OP_ALLGATHER, [g.a(L[k % 2], 1, True, f32x4=True),
+                                             jacc.arg(ALL.data_ptr(), n, J.JACC_F32X4, 2, J.JACC_ARG_DEVICE)])
+            g.add_task(J.JACC_OP_NBODY_STEP_F32, [jacc.arg(ALL.data_ptr(), n, J.JACC_F32X4, 1, J.JACC_ARG_DEVICE),
+                                                   g.a(Vl, 3, True, f32x4=True), g.a(L[(k + 1) % 2], 2, True, f32x4=True)],
+                       jacc.jacc_nbody_params_t(lo, 0.016, 0.01, 1.0))
+        st = g.stats()
+        res["plan"] = (st["h2d_count"], st["d2h_count"], st["collectives"], st["kernels"])
+        g.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception as e:   # surface the error to the parent
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+def test_spmd_world2_gloo():
+    world = 2
+    port = 29500 + (os.getpid() % 1000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert "error" not in out[r], out[r].get("error")
+        assert out[r]["hist"] and out[r]["reduce"] and out[r]["sgemm"] and out[r]["nbody"], out[r]
+        assert out[r]["plan"] == (2, 3, 10, 10), out[r]["plan"]
+
+
+def test_shard_range_partition():
+    import synth
+    for n in (0, 1, 7, 1 << 20, 8192, 131072):
+        for w in (1, 2, 3, 4, 8):
+            rs = [synth.shard_range(n, r, w) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
