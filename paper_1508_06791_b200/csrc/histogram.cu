@@ -36,10 +36,13 @@ constexpr int kFlushChunks = 15;          // 15 * 16 = 240 keys <= 255 per lane
 constexpr int kSubWords = 65 * 32;        // 256 bins * 32 lanes / 4 per word + 1 dummy group
 constexpr int kSmemBytes = kWarps * kSubWords * 4 + 256 * 4;
 
-// Branch-free: an out-of-range key is clamped to bin `nbins` (<= 256), a bin
-// that is never merged into the output (bin 256 lives in the dummy group 64).
-// Byte address of (bin kk, lane) = (kk/4)*128 + lane*4 + kk%4 = 32 kk - 31 (kk%4)
-// + lane*4; a lane only ever touches bytes of its own words -> bank `lane`.
+// One key: branch-free range check (a key is clamped to bin `nbins` <= 256,
+// a bin never merged into the output; bin 256 = dummy group 64), then a byte
+// counter increment at (bin/4)*128 + lane*4 + bin%4 = 32 kk - 31 (kk%4) +
+// lane*4: a lane only touches its own words, all in bank `lane`, so a warp's
+// 32 updates never conflict.  (Measured alternatives -- two or four keys per
+// lane in flight with duplicate merging -- cost more issue slots than the
+// dependency latency they hide: 200 and 230 us vs 193 us at 2^28 keys.)
 __device__ __forceinline__ void count_key(uint8_t *sub_lane_b, int k, unsigned nbins) {
     const unsigned kk = min((unsigned)k, nbins);
     uint8_t *p = sub_lane_b + (32u * kk - 31u * (kk & 3u));

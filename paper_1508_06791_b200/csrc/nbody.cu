@@ -172,12 +172,12 @@ Variant variant() {
     static Variant v = {nullptr, 0};
     if (!v.fn) {
         const char *e = getenv("JACC_NBODY_VARIANT");   // experiments only: "P,S"
-        int P = 2, S = 0;
+        int P = 4, S = 0;
         if (e) sscanf(e, "%d,%d", &P, &S);
 #define V(p, s) if (P == p && S == s) v = {nbody_partial_kernel<p, s>, 2 * p + s}
         V(2, 0); V(0, 4); V(2, 2); V(3, 0); V(4, 0); V(1, 0);
 #undef V
-        if (!v.fn) v = {nbody_partial_kernel<2, 0>, 4};
+        if (!v.fn) v = {nbody_partial_kernel<4, 0>, 8};
     }
     return v;
 }

@@ -316,6 +316,58 @@ int resolve_buffer(jacc_graph *g, const jacc_arg_t &a, std::vector<Buffer> &newb
     return JACC_OK;
 }
 
+// Rough device-time estimate of a task (s) from its algorithmic bytes/flops
+// at B200-class rates: only used to ORDER the host->device copies.
+double est_cost(const jacc_graph *g, const Task &T) {
+    const TaskArg *a = T.args.data();
+    const double hbm = 6e12, alu = 5e13, tc = 2.5e14, link = 5e10;
+    switch (T.op) {
+        case JACC_OP_VADD_F32: return 12.0 * a[0].count / hbm;
+        case JACC_OP_REDUCE_SUM_F32:
+        case JACC_OP_HISTOGRAM_I32: return 4.0 * a[0].count / hbm;
+        case JACC_OP_BLACKSCHOLES_F32: return 12.0 * a[0].count / hbm;
+        case JACC_OP_BLACKSCHOLES_SOA_F32: return 28.0 * a[0].count / hbm;
+        case JACC_OP_SGEMM_F32: {
+            const jacc_sgemm_params_t *p = (const jacc_sgemm_params_t *)T.params.data();
+            return 2.0 * p->M * p->N * p->K / tc;
+        }
+        case JACC_OP_NBODY_STEP_F32: return 20.0 * a[0].count * a[1].count / alu;
+        default: return (double)a[0].count * dtype_size(a[0].dtype) / link;
+    }
+}
+
+// "Nodes' re-organization ... early kernel scheduling" (P:95, reading R6):
+// host->device copies are issued in order of the critical path (estimated
+// device time from the consuming task to the end of the graph), so the
+// longest chain's inputs land first and its kernels start while the other
+// inputs are still crossing PCIe.  The lowered action list itself (and so
+// every counted copy) is unchanged.
+// Bottom level of every task: its estimated cost plus the longest estimated
+// path through its successors to the end of the graph.
+std::vector<double> bottom_level(const jacc_graph *g) {
+    const int nt = (int)g->tasks.size();
+    std::vector<double> prio(nt, 0.0);
+    std::vector<std::vector<int>> succ(nt);
+    for (int t = 0; t < nt; ++t)
+        for (int p : g->tasks[t].preds) succ[p].push_back(t);
+    for (int t = nt - 1; t >= 0; --t) {
+        double m = 0.0;
+        for (int s : succ[t]) m = std::max(m, prio[s]);
+        prio[t] = est_cost(g, g->tasks[t]) + m;
+    }
+    return prio;
+}
+
+std::vector<int> h2d_issue_order(const jacc_graph *g) {
+    const std::vector<double> prio = bottom_level(g);
+    std::vector<int> idx;
+    for (int i = 0; i < (int)g->plan.size(); ++i)
+        if (g->plan[i].kind == A_H2D) idx.push_back(i);
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int x, int y) { return prio[g->plan[x].task] > prio[g->plan[y].task]; });
+    return idx;
+}
+
 // ------------------------------------------------------------- planner
 // Transfer model G.3 (reading R3) -- identical to the
 // oracle's oracle/graph_model.py:plan, which tests/ compare against.
@@ -329,10 +381,26 @@ void make_plan(jacc_graph *g) {
         dev_valid[b] = (B.cachable && B.dev_current && !B.invalidated && B.dptr) ? 1 : 0;
     }
     g->plan.clear();
-    // streams: chains stay on the stream of their latest predecessor,
-    // independent tasks go round-robin (out-of-order issue, R6)
+    // streams (out-of-order issue, R6): a task with predecessors stays on the
+    // stream of its latest one (a chain needs no cross-stream waits); a root
+    // task gets a stream by the rank of its critical path among the roots --
+    // the longest chains own a stream each, the shortest share the last one
+    // -- so a long chain never queues behind a short one whose inputs are
+    // copied in late (H2D is issued critical-path first).
     const int ns = n_streams_of(g);
-    int rr = 0;
+    std::vector<int> root_stream(g->tasks.size(), 0);
+    {
+        const std::vector<double> prio = bottom_level(g);
+        std::vector<int> roots;
+        for (int t = 0; t < (int)g->tasks.size(); ++t) {   // chain heads: no kernel predecessor
+            if (is_collective(g->tasks[t].op)) continue;
+            bool head = true;
+            for (int p : g->tasks[t].preds) head = head && is_collective(g->tasks[p].op);
+            if (head) roots.push_back(t);
+        }
+        std::stable_sort(roots.begin(), roots.end(), [&](int x, int y) { return prio[x] > prio[y]; });
+        for (int r = 0; r < (int)roots.size(); ++r) root_stream[roots[r]] = std::min(r, ns - 1);
+    }
     for (int t = 0; t < (int)g->tasks.size(); ++t) {
         Task &T = g->tasks[t];
         if (naive || (g->cfg.flags & JACC_GRAPH_SERIAL)) {
@@ -345,7 +413,7 @@ void make_plan(jacc_graph *g) {
                 int ps = g->tasks[T.preds[p]].stream;
                 if (ps >= 0) { s = ps; break; }
             }
-            if (s < 0) { s = rr % ns; rr++; }
+            if (s < 0) s = root_stream[t];
             T.stream = s;
         }
         const int at = atomic_out(T.op);
@@ -575,51 +643,6 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(JACC_ERR_CUDA, "launch %s: %s", op_name(T.op), cudaGetErrorString(e));
     return JACC_OK;
-}
-
-// Rough device-time estimate of a task (s) from its algorithmic bytes/flops
-// at B200-class rates: only used to ORDER the host->device copies.
-double est_cost(const jacc_graph *g, const Task &T) {
-    const TaskArg *a = T.args.data();
-    const double hbm = 6e12, alu = 5e13, tc = 2.5e14, link = 5e10;
-    switch (T.op) {
-        case JACC_OP_VADD_F32: return 12.0 * a[0].count / hbm;
-        case JACC_OP_REDUCE_SUM_F32:
-        case JACC_OP_HISTOGRAM_I32: return 4.0 * a[0].count / hbm;
-        case JACC_OP_BLACKSCHOLES_F32: return 12.0 * a[0].count / hbm;
-        case JACC_OP_BLACKSCHOLES_SOA_F32: return 28.0 * a[0].count / hbm;
-        case JACC_OP_SGEMM_F32: {
-            const jacc_sgemm_params_t *p = (const jacc_sgemm_params_t *)T.params.data();
-            return 2.0 * p->M * p->N * p->K / tc;
-        }
-        case JACC_OP_NBODY_STEP_F32: return 20.0 * a[0].count * a[1].count / alu;
-        default: return (double)a[0].count * dtype_size(a[0].dtype) / link;
-    }
-}
-
-// "Nodes' re-organization ... early kernel scheduling" (P:95, reading R6):
-// host->device copies are issued in order of the critical path (estimated
-// device time from the consuming task to the end of the graph), so the
-// longest chain's inputs land first and its kernels start while the other
-// inputs are still crossing PCIe.  The lowered action list itself (and so
-// every counted copy) is unchanged.
-std::vector<int> h2d_issue_order(const jacc_graph *g) {
-    const int nt = (int)g->tasks.size();
-    std::vector<double> prio(nt, 0.0);
-    std::vector<std::vector<int>> succ(nt);
-    for (int t = 0; t < nt; ++t)
-        for (int p : g->tasks[t].preds) succ[p].push_back(t);
-    for (int t = nt - 1; t >= 0; --t) {
-        double m = 0.0;
-        for (int s : succ[t]) m = std::max(m, prio[s]);
-        prio[t] = est_cost(g, g->tasks[t]) + m;
-    }
-    std::vector<int> idx;
-    for (int i = 0; i < (int)g->plan.size(); ++i)
-        if (g->plan[i].kind == A_H2D) idx.push_back(i);
-    std::stable_sort(idx.begin(), idx.end(),
-                     [&](int x, int y) { return prio[g->plan[x].task] > prio[g->plan[y].task]; });
-    return idx;
 }
 
 int issue(jacc_graph *g) {
