@@ -337,6 +337,42 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ main arm
+def cfg1_latency(torch, J, reps=200):
+    """Task-graph time of BASELINE config 1 alone (vadd -> reduce, 2^20 f32):
+    host wall clock per execute+sync, inputs device-resident, direct issue vs
+    plan replay (one CUDA graph launch); and the same graph
+    end to end from pinned host buffers (H2D a, b; D2H c, s every execute)."""
+    from paper_1508_06791_b200.torch_glue import make_graph
+    R, W = J.JACC_READ, J.JACC_WRITE
+    a, b = synth.vadd_inputs()
+    out = {}
+    for mode in ("direct", "replay", "e2e_direct", "e2e_replay"):
+        host = mode.startswith("e2e")
+        flags = J.JACC_GRAPH_REPLAY if mode.endswith("replay") else 0
+        g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=flags)
+        if host:
+            ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+            tc, ts = torch.empty(a.size, pin_memory=True), torch.empty(1, pin_memory=True)
+        else:
+            ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+            tc, ts = torch.empty(a.size, device="cuda"), torch.empty(1, device="cuda")
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R), g.a(tb, R), g.a(tc, W)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(tc, R), g.a(ts, W)])
+        for _ in range(5):
+            g.run()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            g.run()
+        out[mode + "_us"] = (time.perf_counter() - t0) / reps * 1e6
+        st = g.stats()
+        if mode.endswith("replay"):
+            out[mode + "_graph_replays"] = int(st["graph_replays"])
+        g.destroy()
+    out["note"] = "host wall clock per jacc_graph_execute + jacc_graph_sync, mean of %d" % reps
+    return out
+
+
 def run_jacc(args):
     import torch
     import torch.distributed as dist
@@ -436,6 +472,8 @@ def run_jacc(args):
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
             "e2e": e2e, "step_ms": times, "counted_copies_device_resident": {
                 "h2d": int(stats["h2d_count"]), "d2h": int(stats["d2h_count"])}}
+    if world == 1 and not args.no_e2e:
+        line["cfg1_task_graph"] = cfg1_latency(torch, J)
     if not args.no_cpu_baseline and world == 1:
         total, desc, cores, parts = cpu_oracle_sample()
         line["cpu_baseline"] = {"value": 1.0 / total, "unit": UNIT, "cores": cores, "kind": "oracle",

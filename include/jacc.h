@@ -89,6 +89,14 @@ typedef enum jacc_dtype {
                                 lowering), all actions on one stream: the
                                 counted-copies comparison baseline         */
 #define JACC_GRAPH_SERIAL 2u /* one compute stream (no out-of-order issue)   */
+#define JACC_GRAPH_REPLAY 4u /* plan replay: the issued
+                                action list is captured once into a CUDA
+                                graph and re-launched by later executes with
+                                the same plan (one launch instead of one per
+                                action).  A plan that cannot be captured
+                                (e.g. pageable host memory) is issued
+                                directly; stats.graph_captures/replays say
+                                which happened                              */
 
 /* -------------------------------------------------------------- ops */
 typedef enum jacc_op {
@@ -222,6 +230,7 @@ typedef struct jacc_stats {
     int32_t n_tasks, n_buffers;
     int32_t state;      /* 0 BUILDING, 1 EXECUTING, 2 DONE, 3 FAILED       */
     int32_t reserved;
+    uint64_t graph_captures, graph_replays; /* JACC_GRAPH_REPLAY counters   */
 } jacc_stats_t;
 
 /* ------------------------------------------------------------ entry points */

@@ -42,24 +42,36 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// One work unit: kBlock * (2P + S) targets x one chunk of sources.  P target
-// PAIRS use the paired FP32 instructions (FADD2/FFMA2/FMUL2, which run on the
-// FMA-heavy pipe), S further targets use scalar FP32 (which the scheduler can
-// place on the other FP32 pipe): mixing the two keeps both FP32 pipes and the
-// MUFU (rsqrt) busy.  Target k of thread tid is t0 + tid + k * kBlock.
-template <int P, int S>
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// One work unit: kBlock * 2P targets x one chunk of sources.  Every thread
+// holds P target PAIRS and uses the paired FP32 instructions
+// (FADD2/FFMA2/FMUL2, FMA-heavy pipe) -- half the FP32 issue slots of scalar
+// code for the same arithmetic.  Per pair and source, the first P - Q pairs
+// take s = m inv^3 from one rsqrt (2 MUFU.RSQ, 12 paired ops), the last Q
+// pairs from s = 2^(lg2 m - 1.5 lg2 r2) (4 MUFU, 10 paired ops): moving
+// some work from the FP32 pipe to the MUFU balances the two pipes.
+// Target k of thread tid is t0 + tid + k * kBlock.
+template <int P, int Q>
 __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
-    constexpr int T = 2 * P + S;
-    __shared__ float4 tile[2 * kTile];   // per source: (x, x, y, y), (z, z, m, m)
+    constexpr int T = 2 * P;
+    constexpr int TW = Q > 0 ? 3 : 2;     // float4 words per source in the tile
+    __shared__ float4 tile[TW * kTile];   // (x, x, y, y), (z, z, m, m) [, (lg2 m, lg2 m, 0, 0)]
     const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
     const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
     const int64_t j_end = min(j_begin + kChunk, n_src);
-    float2 nx[P > 0 ? P : 1], ny[P > 0 ? P : 1], nz[P > 0 ? P : 1];     // -x of target pairs
-    float2 ax[P > 0 ? P : 1], ay[P > 0 ? P : 1], az[P > 0 ? P : 1];
-    float sx[S > 0 ? S : 1], sy[S > 0 ? S : 1], sz[S > 0 ? S : 1];
-    float bx[S > 0 ? S : 1], by[S > 0 ? S : 1], bz[S > 0 ? S : 1];
+    float2 nx[P], ny[P], nz[P], ax[P], ay[P], az[P];    // nx = -x of the target pair
     auto load_t = [&](int k) {
         const int64_t t = t0 + threadIdx.x + k * kBlock;
         return t < n_tgt ? pos_src[tgt_offset + t] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -70,13 +82,8 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
         nx[p] = f2(-a.x, -b.x); ny[p] = f2(-a.y, -b.y); nz[p] = f2(-a.z, -b.z);
         ax[p] = ay[p] = az[p] = f2(0.f, 0.f);
     }
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-        const float4 a = load_t(2 * P + q);
-        sx[q] = a.x; sy[q] = a.y; sz[q] = a.z;
-        bx[q] = by[q] = bz[q] = 0.f;
-    }
     const float2 e2 = f2(eps2, eps2);
+    const float2 m15 = f2(-1.5f, -1.5f);
     for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
         __syncthreads();
 #pragma unroll
@@ -84,41 +91,43 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
             const int s = threadIdx.x + q * kBlock;
             const int64_t j = j0 + s;
             const float4 v = j < j_end ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-            tile[2 * s] = make_float4(v.x, v.x, v.y, v.y);
-            tile[2 * s + 1] = make_float4(v.z, v.z, v.w, v.w);
+            tile[TW * s] = make_float4(v.x, v.x, v.y, v.y);
+            tile[TW * s + 1] = make_float4(v.z, v.z, v.w, v.w);
+            if (Q > 0) {   // m = 0 (padding) -> 2^-inf = 0: contributes 0
+                const float lm = v.w > 0.f ? lg2_approx(v.w) : -INFINITY;
+                tile[TW * s + 2] = make_float4(lm, lm, 0.f, 0.f);
+            }
         }
         __syncthreads();
-        float2 tx[P > 0 ? P : 1], ty[P > 0 ? P : 1], tz[P > 0 ? P : 1];
-        float ux[S > 0 ? S : 1], uy[S > 0 ? S : 1], uz[S > 0 ? S : 1];
+        float2 tx[P], ty[P], tz[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = f2(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < S; ++q) ux[q] = uy[q] = uz[q] = 0.f;
 #pragma unroll 4
         for (int s = 0; s < kTile; ++s) {
-            const float4 A = tile[2 * s], B = tile[2 * s + 1];
+            const float4 A = tile[TW * s], B = tile[TW * s + 1];
             const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
+            float2 lmj = f2(0.f, 0.f);
+            if (Q > 0) {
+                const float4 C = tile[TW * s + 2];
+                lmj = f2(C.x, C.y);
+            }
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 const float2 dx = __fadd2_rn(xj, nx[p]), dy = __fadd2_rn(yj, ny[p]), dz = __fadd2_rn(zj, nz[p]);
                 float2 r2 = __ffma2_rn(dx, dx, e2);
                 r2 = __ffma2_rn(dy, dy, r2);
                 r2 = __ffma2_rn(dz, dz, r2);
-                const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
-                const float2 sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
+                float2 sc;
+                if (p < P - Q) {
+                    const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+                    sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
+                } else {
+                    const float2 l = __ffma2_rn(f2(lg2_approx(r2.x), lg2_approx(r2.y)), m15, lmj);
+                    sc = f2(ex2_approx(l.x), ex2_approx(l.y));
+                }
                 tx[p] = __ffma2_rn(dx, sc, tx[p]);
                 ty[p] = __ffma2_rn(dy, sc, ty[p]);
                 tz[p] = __ffma2_rn(dz, sc, tz[p]);
-            }
-#pragma unroll
-            for (int q = 0; q < S; ++q) {
-                const float dx = A.x - sx[q], dy = A.z - sy[q], dz = B.x - sz[q];
-                const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
-                const float inv = rsqrt_approx(r2);
-                const float sc = (B.z * inv) * (inv * inv);
-                ux[q] = fmaf(dx, sc, ux[q]);
-                uy[q] = fmaf(dy, sc, uy[q]);
-                uz[q] = fmaf(dz, sc, uz[q]);
             }
         }
 #pragma unroll
@@ -127,8 +136,6 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
             ay[p] = __fadd2_rn(ay[p], ty[p]);
             az[p] = __fadd2_rn(az[p], tz[p]);
         }
-#pragma unroll
-        for (int q = 0; q < S; ++q) { bx[q] += ux[q]; by[q] += uy[q]; bz[q] += uz[q]; }
     }
     float4 *out = part + (int64_t)blockIdx.y * n_tgt;
 #pragma unroll
@@ -136,11 +143,6 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
         const int64_t ta = t0 + threadIdx.x + (2 * p) * kBlock, tb = ta + kBlock;
         if (ta < n_tgt) out[ta] = make_float4(ax[p].x, ay[p].x, az[p].x, 0.f);
         if (tb < n_tgt) out[tb] = make_float4(ax[p].y, ay[p].y, az[p].y, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-        const int64_t t = t0 + threadIdx.x + (2 * P + q) * kBlock;
-        if (t < n_tgt) out[t] = make_float4(bx[q], by[q], bz[q], 0.f);
     }
 }
 
@@ -171,11 +173,11 @@ struct Variant { partial_fn fn; int tpt; };
 Variant variant() {
     static Variant v = {nullptr, 0};
     if (!v.fn) {
-        const char *e = getenv("JACC_NBODY_VARIANT");   // experiments only: "P,S"
-        int P = 4, S = 0;
-        if (e) sscanf(e, "%d,%d", &P, &S);
-#define V(p, s) if (P == p && S == s) v = {nbody_partial_kernel<p, s>, 2 * p + s}
-        V(2, 0); V(0, 4); V(2, 2); V(3, 0); V(4, 0); V(1, 0);
+        const char *e = getenv("JACC_NBODY_VARIANT");   // experiments only: "P,Q"
+        int P = 4, Q = 0;
+        if (e) sscanf(e, "%d,%d", &P, &Q);
+#define V(p, q) if (P == p && Q == q) v = {nbody_partial_kernel<p, q>, 2 * p}
+        V(2, 0); V(4, 0); V(4, 1); V(5, 2); V(3, 1); V(5, 1); V(6, 2);
 #undef V
         if (!v.fn) v = {nbody_partial_kernel<4, 0>, 8};
     }

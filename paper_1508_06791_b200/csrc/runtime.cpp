@@ -133,6 +133,13 @@ struct jacc_graph {
     bool own_h2d = false, own_d2h = false, own_comm = false;
     jacc_stats_t stats;
     int pending_error = JACC_OK;
+    // JACC_GRAPH_REPLAY: captured CUDA graph of the issued action list
+    cudaGraphExec_t exec = nullptr;
+    std::vector<Action> exec_plan;   // the plan `exec` was captured from
+    uint64_t exec_launches = 0;
+    bool exec_failed = false;        // capture impossible for this plan: issue directly
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -715,6 +722,71 @@ int sync_all(jacc_graph *g) {
     return JACC_OK;
 }
 
+bool same_plan(const std::vector<Action> &a, const std::vector<Action> &b) {
+    if (a.size() != b.size()) return false;
+    for (size_t i = 0; i < a.size(); ++i)
+        if (a[i].kind != b[i].kind || a[i].buf != b[i].buf || a[i].task != b[i].task) return false;
+    return true;
+}
+
+// SURVEY §8(f) f2, "plan replay": the first execute of a plan issues its
+// actions under CUDA stream capture (every graph stream forked from
+// compute[0] and joined back), later executes with an identical plan launch
+// the instantiated graph -- one launch instead of one per copy, memset,
+// kernel, event and collective.  Plans that cannot be captured (pageable
+// host memory) are remembered and issued directly.
+int issue_replay(jacc_graph *g) {
+    cudaStream_t origin = g->compute[0];
+    if (g->exec && same_plan(g->exec_plan, g->plan)) {
+        CK(cudaGraphLaunch(g->exec, origin));
+        g->stats.launches = g->exec_launches;
+        g->stats.graph_replays++;
+        return JACC_OK;
+    }
+    if (g->exec_failed && same_plan(g->exec_plan, g->plan)) return issue(g);
+    if (g->exec) {
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+    }
+    std::vector<cudaStream_t> others;
+    for (int i = 1; i < g->n_streams; ++i) others.push_back(g->compute[i]);
+    for (cudaStream_t s : {g->h2d, g->d2h, g->comm})
+        if (s && s != origin && std::find(others.begin(), others.end(), s) == others.end()) others.push_back(s);
+    if (!g->ev_fork) CK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+    while (g->ev_join.size() < others.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g->ev_join.push_back(e);
+    }
+    CK(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed));
+    cudaError_t e = cudaEventRecord(g->ev_fork, origin);
+    for (size_t i = 0; e == cudaSuccess && i < others.size(); ++i) e = cudaStreamWaitEvent(others[i], g->ev_fork, 0);
+    int rc = e == cudaSuccess ? issue(g) : cuda_fail(e, "capture fork");
+    for (size_t i = 0; rc == JACC_OK && i < others.size(); ++i) {
+        e = cudaEventRecord(g->ev_join[i], others[i]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(origin, g->ev_join[i], 0);
+        if (e != cudaSuccess) rc = cuda_fail(e, "capture join");
+    }
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(origin, &graph);
+    if (rc == JACC_OK && e == cudaSuccess && graph)
+        e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    g->exec_plan = g->plan;
+    if (rc != JACC_OK || e != cudaSuccess || !g->exec) {
+        // not capturable (e.g. pageable memcpy): clear the error, issue directly
+        cudaGetLastError();
+        if (g->exec) { cudaGraphExecDestroy(g->exec); g->exec = nullptr; }
+        g->exec_failed = true;
+        return issue(g);
+    }
+    g->exec_failed = false;
+    g->exec_launches = g->stats.launches;
+    g->stats.graph_captures++;
+    CK(cudaGraphLaunch(g->exec, origin));
+    return JACC_OK;
+}
+
 }  // namespace
 
 // ================================================================ ABI
@@ -825,7 +897,9 @@ int jacc_graph_execute(jacc_graph_t *g) {
     plan_counts(g, &g->stats);
     g->have_times = false;
     g->state = ST_EXECUTING;
-    rc = issue(g);
+    rc = (g->cfg.flags & JACC_GRAPH_REPLAY) && !(g->cfg.flags & JACC_GRAPH_NAIVE) && g->cfg.fail_task == 0
+             ? issue_replay(g)
+             : issue(g);
     if (rc != JACC_OK) {
         sync_all(g);   // drain what was issued; no D2H after the failure point
         g->state = ST_FAILED;
@@ -940,6 +1014,9 @@ int jacc_graph_destroy(jacc_graph_t *g) {
         if (g->own_h2d) cudaStreamDestroy(g->h2d);
         if (g->own_d2h) cudaStreamDestroy(g->d2h);
         if (g->own_comm) cudaStreamDestroy(g->comm);
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+        for (cudaEvent_t e : g->ev_join) cudaEventDestroy(e);
     }
     delete g;
     return JACC_OK;
