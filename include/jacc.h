@@ -138,8 +138,42 @@ typedef enum jacc_op {
      *   BROADCAST:     buf:RW [n]; params jacc_bcast_params_t              */
     JACC_OP_ALLREDUCE_SUM = 8,
     JACC_OP_ALLGATHER = 9,
-    JACC_OP_BROADCAST = 10
+    JACC_OP_BROADCAST = 10,
+    /* 2D convolution ("convolves a 2048 x 2048
+     * image with a 5 x 5 filter"; reading R20): true convolution, zero
+     * padding, same-size output,
+     *   out[y][x] = sum_{i,j} f[i][j] img[y + r - i][x + r - j].
+     * args: img:R f32[H*W] (row-major), filter:R f32[(2r+1)^2],
+     * out:W f32[H*W]; params jacc_conv2d_params_t (1 <= r <= 4).           */
+    JACC_OP_CONV2D_F32 = 11,
+    /* Correlation matrix (P:494 OpenBitSet "intersection
+     * count", P:602 `popc`; reading R21):
+     *   C[i][j] = sum_w popcount(A_i[w] & B_j[w]).
+     * args: A:R i32[ta*words] (term bitsets, bit d%32 of word d/32 =
+     * document d), B:R i32[tb*words] (may be the same buffer as A),
+     * C:W i32[ta*tb]; params jacc_corr_params_t.  Bit-exact.                */
+    JACC_OP_CORR_POPC_U32 = 12,
+    /* Sparse matrix-vector product, CSR (R22):
+     *   y[i] = sum_{k=row_ptr[i]}^{row_ptr[i+1]-1} val[k] x[col[k]].
+     * args: row_ptr:R i32[n+1], col:R i32[nnz], val:R f32[nnz],
+     * x:R f32[ncols], y:W f32[n]; params jacc_spmv_params_t.  The caller
+     * guarantees 0 <= row_ptr[i] <= row_ptr[i+1] <= nnz, 0 <= col < ncols. */
+    JACC_OP_SPMV_CSR_F32 = 13
 } jacc_op_t;
+
+typedef struct jacc_corr_params {
+    int64_t ta, tb, words;  /* terms of A, terms of B, 32-bit words per term   */
+} jacc_corr_params_t;
+
+typedef struct jacc_spmv_params {
+    int64_t n, ncols;       /* rows, columns                                  */
+} jacc_spmv_params_t;
+
+typedef struct jacc_conv2d_params {
+    int64_t H, W;       /* image rows, columns                                 */
+    int32_t radius;     /* filter is (2 radius + 1)^2, radius in [1, 4]        */
+    int32_t reserved;
+} jacc_conv2d_params_t;
 
 typedef struct jacc_hist_params {
     int32_t nbins;      /* 1 .. 4096 (the sm_100a fast path is nbins <= 256) */

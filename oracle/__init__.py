@@ -72,6 +72,10 @@ def lib():
             L.oracle_nbody_accel.argtypes = [_F64P, _i64, _I64P, _i64, _f64, _f64, _F64P]
             L.oracle_nbody_steps.argtypes = [_F64P, _F64P, _i64, ctypes.c_int, _f64, _f64,
                                              _f64, _F64P, _I64P]
+            L.oracle_conv2d_f32.argtypes = [_F32P, _i64, _i64, _F32P, ctypes.c_int, _F64P, _F64P]
+            _U32P = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+            L.oracle_corr_popc.argtypes = [_U32P, _i64, _U32P, _i64, _i64, _I32P]
+            L.oracle_spmv_csr_f32.argtypes = [_I32P, _I32P, _F32P, _F32P, _i64, _F64P, _F64P]
             _lib = L
     return _lib
 
@@ -185,3 +189,38 @@ def nbody_steps(pos, vel, steps: int, dt: float = 0.016, eps2: float = 0.01, G: 
     tgt = np.arange(n, dtype=np.int64)
     lib().oracle_nbody_steps(p, v, n, int(steps), dt, eps2, G, scratch, tgt)
     return p, v
+
+
+def conv2d(img, filt):
+    """fp64 (out, sum|f||img|): zero-padded true 2D convolution, same size
+    (reading R20)."""
+    img = _c(img, np.float32)
+    filt = _c(filt, np.float32)
+    H, W = img.shape
+    k = filt.shape[0]
+    assert filt.shape == (k, k) and k % 2 == 1
+    out = np.empty((H, W), np.float64)
+    ab = np.empty((H, W), np.float64)
+    lib().oracle_conv2d_f32(img, H, W, filt, k // 2, out, ab)
+    return out, ab
+
+
+def corr_popc(A, B=None):
+    """C[i][j] = sum_w popcount(A[i][w] & B[j][w]) (R21).
+    A: (ta, words) uint32 bitsets; B defaults to A."""
+    A = _c(A, np.uint32)
+    B = A if B is None else _c(B, np.uint32)
+    assert A.shape[1] == B.shape[1]
+    C = np.empty((A.shape[0], B.shape[0]), np.int32)
+    lib().oracle_corr_popc(A, A.shape[0], B, B.shape[0], A.shape[1], C)
+    return C
+
+
+def spmv_csr(row_ptr, col, val, x):
+    """fp64 (y, sum|a x|) with y = A x, A in CSR (R22)."""
+    rp = _c(row_ptr, np.int32); cl = _c(col, np.int32)
+    v = _c(val, np.float32); xx = _c(x, np.float32)
+    n = rp.size - 1
+    y = np.empty(n, np.float64); ab = np.empty(n, np.float64)
+    lib().oracle_spmv_csr_f32(rp, cl, v, xx, n, y, ab)
+    return y, ab

@@ -43,6 +43,9 @@ OPS = {
     "allreduce": ((READWRITE,),),
     "allgather": ((READ,), (WRITE,)),
     "broadcast": ((READWRITE,),),
+    "conv2d": ((READ,), (READ,), (WRITE,)),
+    "corr": ((READ,), (READ,), (WRITE,)),
+    "spmv": ((READ,),) * 4 + ((WRITE,),),
 }
 ATOMIC_OUT = {"reduce": 1, "hist": 1}   # arg index of the @Atomic(op=ADD) output
 COLLECTIVES = {"allreduce", "allgather", "broadcast"}

@@ -218,3 +218,79 @@ void oracle_nbody_steps(double *pos, double *vel, int64_t n, int steps,
         }
     }
 }
+
+/* ---------------------------------------------------------------------
+ * 2D convolution ("convolves a 2048 x 2048
+ * image with a 5 x 5 filter").  Reading R20: true convolution (the filter
+ * is flipped), zero padding outside the image, output the size of the image:
+ *   out[y][x] = sum_{i=0}^{2r} sum_{j=0}^{2r} f[i][j] img[y + r - i][x + r - j]
+ * accumulated in fp64 over i then j.  Also returns, per output, the scale
+ * sum |f[i][j]| |img[...]| the tolerance is expressed in (abs_out may be NULL).
+ * ------------------------------------------------------------------- */
+void oracle_conv2d_f32(const float *img, int64_t H, int64_t W, const float *f, int r,
+                       double *out, double *abs_out) {
+    const int k = 2 * r + 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t y = 0; y < H; ++y) {
+        for (int64_t x = 0; x < W; ++x) {
+            double s = 0.0, a = 0.0;
+            for (int i = 0; i < k; ++i) {
+                const int64_t yy = y + r - i;
+                if (yy < 0 || yy >= H) continue;
+                for (int j = 0; j < k; ++j) {
+                    const int64_t xx = x + r - j;
+                    if (xx < 0 || xx >= W) continue;
+                    const double p = (double)f[i * k + j] * (double)img[yy * W + xx];
+                    s += p;
+                    a += fabs(p);
+                }
+            }
+            out[y * W + x] = s;
+            if (abs_out) abs_out[y * W + x] = a;
+        }
+    }
+}
+
+/* ---------------------------------------------------------------------
+ * Correlation matrix ("the Lucene OpenBitSet
+ * 'intersection count' ... 1024 Terms and 16384 Documents"; "popc").
+ * Reading R21: term t is a bitset over the documents, stored as `words`
+ * 32-bit words (bit d%32 of word d/32 = document d);
+ *   C[i][j] = #{documents in both A_i and B_j} = sum_w popcount(A_i[w] & B_j[w]).
+ * Bits are counted one by one (no builtin), the literal definition.
+ * ------------------------------------------------------------------- */
+void oracle_corr_popc(const uint32_t *A, int64_t ta, const uint32_t *B, int64_t tb,
+                      int64_t words, int32_t *C) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < ta; ++i)
+        for (int64_t j = 0; j < tb; ++j) {
+            int64_t c = 0;
+            for (int64_t w = 0; w < words; ++w) {
+                uint32_t v = A[i * words + w] & B[j * words + w];
+                for (int b = 0; b < 32; ++b) c += (v >> b) & 1u;
+            }
+            C[i * tb + j] = (int32_t)c;
+        }
+}
+
+/* ---------------------------------------------------------------------
+ * Sparse matrix-vector multiply, CSR ("a 44609 x
+ * 44609 matrix with 1029655 non-zeros (The bcsstk32 matrix from Matrix
+ * Market)").  Reading R22: y = A x, A in CSR (row_ptr[n+1], col[nnz],
+ * val[nnz]); y[i] = sum_{k=row_ptr[i]}^{row_ptr[i+1]-1} val[k] x[col[k]] in
+ * fp64 in k order; abs_out[i] = sum |val[k] x[col[k]]| (tolerance scale).
+ * ------------------------------------------------------------------- */
+void oracle_spmv_csr_f32(const int32_t *row_ptr, const int32_t *col, const float *val,
+                         const float *x, int64_t n, double *y, double *abs_out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0, a = 0.0;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+            double p = (double)val[k] * (double)x[col[k]];
+            s += p;
+            a += fabs(p);
+        }
+        y[i] = s;
+        if (abs_out) abs_out[i] = a;
+    }
+}

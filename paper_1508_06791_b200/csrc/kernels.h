@@ -45,4 +45,16 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
                            int64_t n_tgt, const jacc_nbody_params_t *p, void *ws,
                            const jacc_schedule_t *s, cudaStream_t st, int *launches);
 
+// 2D convolution
+cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,
+                       cudaStream_t st, int *launches);
+
+// correlation matrix
+cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int64_t tb, int64_t words, int32_t *C,
+                          cudaStream_t st, int *launches);
+
+// SpMV CSR
+cudaError_t spmv_csr_f32(const int32_t *row_ptr, const int32_t *col, const float *val, const float *x, float *y,
+                         int64_t n, cudaStream_t st, int *launches);
+
 }  // namespace jacc_k

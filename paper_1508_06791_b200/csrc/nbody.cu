@@ -6,20 +6,22 @@
 // tgt_offset .. tgt_offset + n_tgt - 1 (a rank's shard in SPMD, R17).
 //
 // sm_100a design (FP32-pipe bound: 12 fp32 ops + 1 MUFU.RSQ per interaction):
-//   * work unit = (256 targets) x (one chunk of kChunk = 8192 sources); the
-//     chunk size depends on nothing but the source count, so every rank of a
-//     sharded run sums a target's sources in exactly the same groups as one
-//     GPU does (bitwise shard invariance, §8(e)), and 2^17 bodies give 8192
-//     units -- 55 per SM, so the 148 SMs finish within 2% of each other;
-//   * sources stream through shared memory in tiles; each thread holds
-//     kTpt = 4 targets in registers, so one shared-memory load of a source
-//     feeds 4 interactions;
+//   * work unit = (64 threads x 8 targets) x (one chunk of kChunk = 8192
+//     sources); the chunk size depends on nothing but the source count, so
+//     every rank of a sharded run sums a target's sources in exactly the same
+//     groups as one GPU does (bitwise shard invariance, §8(e)), and 2^17
+//     bodies give 4096 units -- 27.7 per SM, the 148 SMs finish together;
+//   * sources stream through shared memory in tiles of 256, stored
+//     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
+//     pairs of the paired FP32 instructions;
+//   * each thread holds 4 target PAIRS in registers and uses the sm_100
+//     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops + 2 MUFU.RSQ per
+//     pair and source, half the FP32 issue slots of scalar code;
+//     measured alternatives (scalar FP32 on the other pipe for some targets,
+//     an lg2/ex2 path that moves work to the MUFU) were slower;
 //   * accumulation is TILE-PARTIAL (each tile summed separately, then added
 //     in tile order), chunk partials go to a workspace and a second kernel
 //     adds the chunks in order and applies kick + drift;
-//   * the x2 variant packs 2 targets per register pair and uses the sm_100
-//     paired FP32 instructions (FADD2 / FFMA2 / FMUL2): half the FP32 issue
-//     slots for the same arithmetic;
 //   * the self term is included: x_j - x_i = 0 with eps2 > 0 contributes 0;
 //     padding sources (j >= n_src) have m = 0 at the origin (contribute 0).
 #include <cstdio>
@@ -42,32 +44,18 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-__device__ __forceinline__ float lg2_approx(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 // One work unit: kBlock * 2P targets x one chunk of sources.  Every thread
 // holds P target PAIRS and uses the paired FP32 instructions
 // (FADD2/FFMA2/FMUL2, FMA-heavy pipe) -- half the FP32 issue slots of scalar
-// code for the same arithmetic.  Per pair and source, the first P - Q pairs
-// take s = m inv^3 from one rsqrt (2 MUFU.RSQ, 12 paired ops), the last Q
-// pairs from s = 2^(lg2 m - 1.5 lg2 r2) (4 MUFU, 10 paired ops): moving
-// some work from the FP32 pipe to the MUFU balances the two pipes.
-// Target k of thread tid is t0 + tid + k * kBlock.
-template <int P, int Q>
+// code for the same arithmetic: per pair and source 12 paired ops + 2
+// MUFU.RSQ.  Target k of thread tid is t0 + tid + k * kBlock.
+template <int P>
 __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
     constexpr int T = 2 * P;
-    constexpr int TW = Q > 0 ? 3 : 2;     // float4 words per source in the tile
-    __shared__ float4 tile[TW * kTile];   // (x, x, y, y), (z, z, m, m) [, (lg2 m, lg2 m, 0, 0)]
+    constexpr int TW = 2;                 // float4 words per source in the tile
+    __shared__ float4 tile[TW * kTile];   // (x, x, y, y), (z, z, m, m)
     const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
     const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
     const int64_t j_end = min(j_begin + kChunk, n_src);
@@ -83,7 +71,6 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
         ax[p] = ay[p] = az[p] = f2(0.f, 0.f);
     }
     const float2 e2 = f2(eps2, eps2);
-    const float2 m15 = f2(-1.5f, -1.5f);
     for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
         __syncthreads();
 #pragma unroll
@@ -93,10 +80,6 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
             const float4 v = j < j_end ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
             tile[TW * s] = make_float4(v.x, v.x, v.y, v.y);
             tile[TW * s + 1] = make_float4(v.z, v.z, v.w, v.w);
-            if (Q > 0) {   // m = 0 (padding) -> 2^-inf = 0: contributes 0
-                const float lm = v.w > 0.f ? lg2_approx(v.w) : -INFINITY;
-                tile[TW * s + 2] = make_float4(lm, lm, 0.f, 0.f);
-            }
         }
         __syncthreads();
         float2 tx[P], ty[P], tz[P];
@@ -106,25 +89,14 @@ __global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__r
         for (int s = 0; s < kTile; ++s) {
             const float4 A = tile[TW * s], B = tile[TW * s + 1];
             const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
-            float2 lmj = f2(0.f, 0.f);
-            if (Q > 0) {
-                const float4 C = tile[TW * s + 2];
-                lmj = f2(C.x, C.y);
-            }
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 const float2 dx = __fadd2_rn(xj, nx[p]), dy = __fadd2_rn(yj, ny[p]), dz = __fadd2_rn(zj, nz[p]);
                 float2 r2 = __ffma2_rn(dx, dx, e2);
                 r2 = __ffma2_rn(dy, dy, r2);
                 r2 = __ffma2_rn(dz, dz, r2);
-                float2 sc;
-                if (p < P - Q) {
-                    const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
-                    sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
-                } else {
-                    const float2 l = __ffma2_rn(f2(lg2_approx(r2.x), lg2_approx(r2.y)), m15, lmj);
-                    sc = f2(ex2_approx(l.x), ex2_approx(l.y));
-                }
+                const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+                const float2 sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
                 tx[p] = __ffma2_rn(dx, sc, tx[p]);
                 ty[p] = __ffma2_rn(dy, sc, ty[p]);
                 tz[p] = __ffma2_rn(dz, sc, tz[p]);
@@ -173,13 +145,11 @@ struct Variant { partial_fn fn; int tpt; };
 Variant variant() {
     static Variant v = {nullptr, 0};
     if (!v.fn) {
-        const char *e = getenv("JACC_NBODY_VARIANT");   // experiments only: "P,Q"
-        int P = 4, Q = 0;
-        if (e) sscanf(e, "%d,%d", &P, &Q);
-#define V(p, q) if (P == p && Q == q) v = {nbody_partial_kernel<p, q>, 2 * p}
-        V(2, 0); V(4, 0); V(4, 1); V(5, 2); V(3, 1); V(5, 1); V(6, 2);
-#undef V
-        if (!v.fn) v = {nbody_partial_kernel<4, 0>, 8};
+        // pairs per thread; 4 measured best on B200 (6.83 ms vs 6.94 ms for 2
+        // at 2^17 bodies).  JACC_NBODY_PAIRS overrides it for experiments.
+        const char *e = getenv("JACC_NBODY_PAIRS");
+        const int P = e ? atoi(e) : 4;
+        v = P == 2 ? Variant{nbody_partial_kernel<2>, 4} : Variant{nbody_partial_kernel<4>, 8};
     }
     return v;
 }

@@ -58,6 +58,9 @@ const char *op_name(int op) {
         case JACC_OP_ALLREDUCE_SUM: return "allreduce";
         case JACC_OP_ALLGATHER: return "allgather";
         case JACC_OP_BROADCAST: return "broadcast";
+        case JACC_OP_CONV2D_F32: return "conv2d";
+        case JACC_OP_CORR_POPC_U32: return "corr";
+        case JACC_OP_SPMV_CSR_F32: return "spmv";
         default: return "?";
     }
 }
@@ -102,7 +105,8 @@ struct Task {
     int stream = 0;           // planned stream index (-1 = comm stream)
     void *ws = nullptr;
     size_t ws_bytes = 0;
-    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;   // timing
+    cudaEvent_t ev_dep = nullptr;                       // dependency (no timing)
     float ms = 0.f;
 };
 
@@ -140,6 +144,8 @@ struct jacc_graph {
     bool exec_failed = false;        // capture impossible for this plan: issue directly
     cudaEvent_t ev_fork = nullptr;
     std::vector<cudaEvent_t> ev_join;
+    bool capturing = false;          // issue() runs under stream capture
+    bool last_was_replay = false;    // current execute = one graph launch on compute[0]
 };
 
 // ---------------------------------------------------------------- helpers
@@ -274,6 +280,40 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             if (root < 0 || root >= g->cfg.world) return fail(JACC_ERR_INVALID_ARG, "broadcast: root");
             break;
         }
+        case JACC_OP_CONV2D_F32: {
+            T(need(3)); T(acc(0, R)); T(acc(1, R)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_F32));
+            if (!params || psz < sizeof(jacc_conv2d_params_t)) return fail(JACC_ERR_INVALID_ARG, "conv2d: params");
+            const jacc_conv2d_params_t *p = (const jacc_conv2d_params_t *)params;
+            if (p->radius < 1 || p->radius > 4) return fail(JACC_ERR_UNSUPPORTED, "conv2d: radius %d", p->radius);
+            const uint64_t k = 2 * p->radius + 1;
+            if (p->H < 0 || p->W < 0 || a[0].count != (uint64_t)(p->H * p->W) || a[2].count != a[0].count ||
+                a[1].count != k * k)
+                return fail(JACC_ERR_INVALID_ARG, "conv2d: counts do not match H x W / filter size");
+            break;
+        }
+        case JACC_OP_CORR_POPC_U32: {
+            T(need(3)); T(acc(0, R)); T(acc(1, R)); T(acc(2, W));
+            for (int i = 0; i < 3; ++i) T(dt(i, JACC_I32));
+            if (!params || psz < sizeof(jacc_corr_params_t)) return fail(JACC_ERR_INVALID_ARG, "corr: params");
+            const jacc_corr_params_t *p = (const jacc_corr_params_t *)params;
+            if (p->ta < 0 || p->tb < 0 || p->words < 0 || a[0].count != (uint64_t)(p->ta * p->words) ||
+                a[1].count != (uint64_t)(p->tb * p->words) || a[2].count != (uint64_t)(p->ta * p->tb))
+                return fail(JACC_ERR_INVALID_ARG, "corr: counts do not match ta, tb, words");
+            break;
+        }
+        case JACC_OP_SPMV_CSR_F32: {
+            T(need(5));
+            for (int i = 0; i < 4; ++i) T(acc(i, R));
+            T(acc(4, W)); T(dt(0, JACC_I32)); T(dt(1, JACC_I32)); T(dt(2, JACC_F32)); T(dt(3, JACC_F32));
+            T(dt(4, JACC_F32));
+            if (!params || psz < sizeof(jacc_spmv_params_t)) return fail(JACC_ERR_INVALID_ARG, "spmv: params");
+            const jacc_spmv_params_t *p = (const jacc_spmv_params_t *)params;
+            if (p->n < 0 || a[0].count != (uint64_t)p->n + 1 || a[1].count != a[2].count ||
+                a[3].count != (uint64_t)p->ncols || a[4].count != (uint64_t)p->n)
+                return fail(JACC_ERR_INVALID_ARG, "spmv: counts do not match n, ncols, nnz");
+            break;
+        }
         default:
             return fail(JACC_ERR_INVALID_ARG, "unknown op %d", op);
     }
@@ -339,6 +379,12 @@ double est_cost(const jacc_graph *g, const Task &T) {
             return 2.0 * p->M * p->N * p->K / tc;
         }
         case JACC_OP_NBODY_STEP_F32: return 20.0 * a[0].count * a[1].count / alu;
+        case JACC_OP_CONV2D_F32: return 8.0 * a[0].count / hbm;
+        case JACC_OP_CORR_POPC_U32: {
+            const jacc_corr_params_t *p = (const jacc_corr_params_t *)T.params.data();
+            return 3.0 * p->ta * p->tb * p->words / alu;
+        }
+        case JACC_OP_SPMV_CSR_F32: return 12.0 * a[1].count / hbm;
         default: return (double)a[0].count * dtype_size(a[0].dtype) / link;
     }
 }
@@ -553,6 +599,7 @@ int prepare_memory(jacc_graph *g) {
     for (Task &T : g->tasks) {
         if (!T.ev_start) CK(cudaEventCreate(&T.ev_start));
         if (!T.ev_end) CK(cudaEventCreate(&T.ev_end));
+        if (!T.ev_dep) CK(cudaEventCreateWithFlags(&T.ev_dep, cudaEventDisableTiming));
         size_t need = 0;
         const TaskArg *a = T.args.data();
         switch (T.op) {
@@ -621,6 +668,23 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
                                        (int64_t)a[1].count, (const jacc_nbody_params_t *)T.params.data(), T.ws, sched,
                                        st, launches);
             break;
+        case JACC_OP_CONV2D_F32: {
+            const jacc_conv2d_params_t *cp = (const jacc_conv2d_params_t *)T.params.data();
+            e = jacc_k::conv2d_f32((const float *)P(0), cp->H, cp->W, (const float *)P(1), cp->radius, (float *)P(2),
+                                   st, launches);
+            break;
+        }
+        case JACC_OP_CORR_POPC_U32: {
+            const jacc_corr_params_t *cp = (const jacc_corr_params_t *)T.params.data();
+            e = jacc_k::corr_popc_u32((const uint32_t *)P(0), cp->ta, (const uint32_t *)P(1), cp->tb, cp->words,
+                                      (int32_t *)P(2), st, launches);
+            break;
+        }
+        case JACC_OP_SPMV_CSR_F32:
+            e = jacc_k::spmv_csr_f32((const int32_t *)P(0), (const int32_t *)P(1), (const float *)P(2),
+                                     (const float *)P(3), (float *)P(4),
+                                     ((const jacc_spmv_params_t *)T.params.data())->n, st, launches);
+            break;
         case JACC_OP_ALLREDUCE_SUM:
         case JACC_OP_ALLGATHER:
         case JACC_OP_BROADCAST: {
@@ -684,9 +748,12 @@ int issue(jacc_graph *g) {
                 if (h2d_issued[a.buf] && g->h2d != st) CK(cudaStreamWaitEvent(st, g->bufs[a.buf].ev_h2d, 0));
             for (int p : T.preds) {
                 const Task &Pt = g->tasks[p];
-                if (stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_end, 0));
+                if (stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_dep, 0));
             }
-            CK(cudaEventRecord(T.ev_start, st));
+            // timing events: under CUDA-graph capture they must be EXTERNAL
+            // record nodes (a plain record is only a capture dependency)
+            CK(g->capturing ? cudaEventRecordWithFlags(T.ev_start, st, cudaEventRecordExternal)
+                            : cudaEventRecord(T.ev_start, st));
             // MEMSET0 actions of this task (auto-zero of @Atomic outputs)
             for (size_t bj = ai; bj-- > 0;) {
                 const Action &M = g->plan[bj];
@@ -696,13 +763,15 @@ int issue(jacc_graph *g) {
             }
             int rc = launch_task(g, T, st, &launches);
             if (rc != JACC_OK) return rc;
-            CK(cudaEventRecord(T.ev_end, st));
+            CK(g->capturing ? cudaEventRecordWithFlags(T.ev_end, st, cudaEventRecordExternal)
+                            : cudaEventRecord(T.ev_end, st));
+            CK(cudaEventRecord(T.ev_dep, st));   // cross-stream dependency marker
             task_done[A.task] = 1;
         } else if (A.kind == A_D2H) {
             Buffer &B = g->bufs[A.buf];
             const Task &W = g->tasks[A.task];
             cudaStream_t ws = stream_of(g, W);
-            if (ws != g->d2h) CK(cudaStreamWaitEvent(g->d2h, W.ev_end, 0));
+            if (ws != g->d2h) CK(cudaStreamWaitEvent(g->d2h, W.ev_dep, 0));
             CK(cudaMemcpyAsync((void *)B.host, B.dptr, B.bytes, cudaMemcpyDeviceToHost, g->d2h));
         }
         // A_MEMSET0 is issued with its task's kernel (same stream)
@@ -714,10 +783,14 @@ int issue(jacc_graph *g) {
 int sync_all(jacc_graph *g) {
     cudaError_t first = cudaSuccess;
     auto chk = [&](cudaError_t e) { if (e != cudaSuccess && first == cudaSuccess) first = e; };
-    for (int i = 0; i < g->n_streams; ++i) chk(cudaStreamSynchronize(g->compute[i]));
-    if (g->h2d) chk(cudaStreamSynchronize(g->h2d));
-    if (g->comm) chk(cudaStreamSynchronize(g->comm));
-    if (g->d2h) chk(cudaStreamSynchronize(g->d2h));
+    if (g->last_was_replay) {   // the graph launch joined every stream into compute[0]
+        chk(cudaStreamSynchronize(g->compute[0]));
+    } else {
+        for (int i = 0; i < g->n_streams; ++i) chk(cudaStreamSynchronize(g->compute[i]));
+        if (g->h2d) chk(cudaStreamSynchronize(g->h2d));
+        if (g->comm && g->comm != g->h2d) chk(cudaStreamSynchronize(g->comm));
+        if (g->d2h && g->d2h != g->h2d) chk(cudaStreamSynchronize(g->d2h));
+    }
     if (first != cudaSuccess) return cuda_fail(first, "sync");
     return JACC_OK;
 }
@@ -761,7 +834,9 @@ int issue_replay(jacc_graph *g) {
     CK(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed));
     cudaError_t e = cudaEventRecord(g->ev_fork, origin);
     for (size_t i = 0; e == cudaSuccess && i < others.size(); ++i) e = cudaStreamWaitEvent(others[i], g->ev_fork, 0);
+    g->capturing = true;
     int rc = e == cudaSuccess ? issue(g) : cuda_fail(e, "capture fork");
+    g->capturing = false;
     for (size_t i = 0; rc == JACC_OK && i < others.size(); ++i) {
         e = cudaEventRecord(g->ev_join[i], others[i]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(origin, g->ev_join[i], 0);
@@ -819,6 +894,7 @@ size_t jacc_abi_sizeof(const char *name) {
 #define S(T) if (!strcmp(name, #T)) return sizeof(T)
     S(jacc_arg_t); S(jacc_schedule_t); S(jacc_config_t); S(jacc_stats_t);
     S(jacc_hist_params_t); S(jacc_sgemm_params_t); S(jacc_nbody_params_t); S(jacc_bcast_params_t);
+    S(jacc_conv2d_params_t); S(jacc_corr_params_t); S(jacc_spmv_params_t);
 #undef S
     return 0;
 }
@@ -897,9 +973,14 @@ int jacc_graph_execute(jacc_graph_t *g) {
     plan_counts(g, &g->stats);
     g->have_times = false;
     g->state = ST_EXECUTING;
-    rc = (g->cfg.flags & JACC_GRAPH_REPLAY) && !(g->cfg.flags & JACC_GRAPH_NAIVE) && g->cfg.fail_task == 0
-             ? issue_replay(g)
-             : issue(g);
+    g->last_was_replay = false;
+    if ((g->cfg.flags & JACC_GRAPH_REPLAY) && !(g->cfg.flags & JACC_GRAPH_NAIVE) && g->cfg.fail_task == 0) {
+        const uint64_t before = g->stats.graph_replays + g->stats.graph_captures;
+        rc = issue_replay(g);
+        g->last_was_replay = rc == JACC_OK && g->stats.graph_replays + g->stats.graph_captures > before;
+    } else {
+        rc = issue(g);
+    }
     if (rc != JACC_OK) {
         sync_all(g);   // drain what was issued; no D2H after the failure point
         g->state = ST_FAILED;
@@ -1008,6 +1089,7 @@ int jacc_graph_destroy(jacc_graph_t *g) {
             dev_free(g, T.ws, T.ws_bytes);
             if (T.ev_start) cudaEventDestroy(T.ev_start);
             if (T.ev_end) cudaEventDestroy(T.ev_end);
+            if (T.ev_dep) cudaEventDestroy(T.ev_dep);
         }
         if (g->own_compute)
             for (int i = 0; i < g->n_streams; ++i) cudaStreamDestroy(g->compute[i]);

@@ -177,7 +177,8 @@ constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quarter, 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-                       float *__restrict__ C, int64_t M, int64_t N, int64_t ldc, int num_kb) {
+                       float *__restrict__ C, int64_t M, int64_t N, int64_t ldc, int num_kb, int num_m,
+                       int num_n) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + kStages * kStageBytes);
@@ -185,7 +186,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full_bar0 = smem_u32(bars), empty_bar0 = smem_u32(bars + kStages),
                    tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m_blk = blockIdx.y, n_blk = blockIdx.x;
+    // Grouped raster: consecutive CTAs walk kGroupM M-tiles for each N-tile,
+    // so a wave of 148 CTAs touches ~16 M-strips x ~9 N-strips of A/B instead
+    // of ~5 M-strips x all 32 N-strips (B re-read from HBM every wave).
+    constexpr int kGroupM = 16;
+    const int pid = blockIdx.x;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int m_blk = first_m + (pid % per_group) % gm;
+    const int n_blk = (pid % per_group) / gm;
     const int nchunks = (num_kb + kChunkKB - 1) / kChunkKB;
 
     if (warp == 0 && lane == 0) {
@@ -370,9 +380,9 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)(Np / BN), (unsigned)(Mp / BM));
-    gemm_3xtf32_kernel<<<grid, kThreads, kSmemBytes, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc,
-                                                           (int)(Kp / BK));
+    const int num_m = (int)(Mp / BM), num_n = (int)(Np / BN);
+    gemm_3xtf32_kernel<<<num_m * num_n, kThreads, kSmemBytes, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc,
+                                                           (int)(Kp / BK), num_m, num_n);
     ++*launches;
     return cudaGetLastError();
 }

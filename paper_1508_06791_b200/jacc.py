@@ -35,7 +35,8 @@ JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY = 1, 2, 4
 JACC_MAX_STREAMS = 8
 (JACC_OP_VADD_F32, JACC_OP_REDUCE_SUM_F32, JACC_OP_HISTOGRAM_I32, JACC_OP_BLACKSCHOLES_F32,
  JACC_OP_BLACKSCHOLES_SOA_F32, JACC_OP_SGEMM_F32, JACC_OP_NBODY_STEP_F32, JACC_OP_ALLREDUCE_SUM,
- JACC_OP_ALLGATHER, JACC_OP_BROADCAST) = range(1, 11)
+ JACC_OP_ALLGATHER, JACC_OP_BROADCAST, JACC_OP_CONV2D_F32, JACC_OP_CORR_POPC_U32,
+ JACC_OP_SPMV_CSR_F32) = range(1, 14)
 JACC_SGEMM_3XTF32, JACC_SGEMM_FFMA = 0, 1
 STATE_NAMES = {0: "BUILDING", 1: "EXECUTING", 2: "DONE", 3: "FAILED"}
 DTYPE_SIZE = {JACC_F32: 4, JACC_I32: 4, JACC_F32X4: 16}
@@ -97,10 +98,24 @@ class jacc_bcast_params_t(ctypes.Structure):
     _fields_ = [("root", ctypes.c_int32)]
 
 
-STRUCTS = {"jacc_arg_t": jacc_arg_t, "jacc_schedule_t": jacc_schedule_t, "jacc_config_t": jacc_config_t,
+class jacc_conv2d_params_t(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int64), ("W", ctypes.c_int64), ("radius", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class jacc_corr_params_t(ctypes.Structure):
+    _fields_ = [("ta", ctypes.c_int64), ("tb", ctypes.c_int64), ("words", ctypes.c_int64)]
+
+
+class jacc_spmv_params_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("ncols", ctypes.c_int64)]
+
+
+STRUCTS = {"jacc_corr_params_t": jacc_corr_params_t, "jacc_spmv_params_t": jacc_spmv_params_t,
+           "jacc_arg_t": jacc_arg_t, "jacc_schedule_t": jacc_schedule_t, "jacc_config_t": jacc_config_t,
            "jacc_stats_t": jacc_stats_t, "jacc_hist_params_t": jacc_hist_params_t,
            "jacc_sgemm_params_t": jacc_sgemm_params_t, "jacc_nbody_params_t": jacc_nbody_params_t,
-           "jacc_bcast_params_t": jacc_bcast_params_t}
+           "jacc_bcast_params_t": jacc_bcast_params_t, "jacc_conv2d_params_t": jacc_conv2d_params_t}
 
 # ------------------------------------------------------------- entry points
 _vp = ctypes.c_void_p

@@ -76,6 +76,29 @@ def main():
                                                    g.a(D(np.zeros_like(pos)), W, f32x4=True)],
                        jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
             units, kind = 20 * n * n, "TFLOP/s"
+        elif op == "conv2d":
+            n = a.n or 2048
+            img = synth.uniform_f32(n * n, 11, -1, 1).reshape(n, n)
+            f = synth.uniform_f32(25, 12, -1, 1).reshape(5, 5)
+            g.add_task(J.JACC_OP_CONV2D_F32, [g.a(D(img), R), g.a(D(f), R), g.a(D(np.zeros_like(img)), W)],
+                       jacc.jacc_conv2d_params_t(n, n, 2, 0))
+            units, kind = 8 * n * n, "GB/s"
+        elif op == "corr":
+            A = synth.corr_bitsets()
+            C = np.zeros((A.shape[0], A.shape[0]), np.int32)
+            g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(D(A.view(np.int32)), R), g.a(D(A.view(np.int32) + 0), R),
+                                                  g.a(D(C), W)],
+                       jacc.jacc_corr_params_t(A.shape[0], A.shape[0], A.shape[1]))
+            n = A.shape[0]
+            units, kind = n * n * A.shape[1] * 32 * 2, "TFLOP/s"   # bit-ops: AND + count per bit pair
+        elif op == "spmv":
+            rp, col, val = synth.banded_csr()
+            n = rp.size - 1
+            x = synth.uniform_f32(n, 5, -1, 1)
+            g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(D(rp), R), g.a(D(col), R), g.a(D(val), R), g.a(D(x), R),
+                                                 g.a(D(np.zeros(n, np.float32)), W)],
+                       jacc.jacc_spmv_params_t(n, n))
+            units, kind = 8 * col.size + 4 * (n + 1) + 8 * n, "GB/s"
         else:
             raise SystemExit(f"unknown op {op}")
         ms = []

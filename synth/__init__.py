@@ -124,3 +124,40 @@ def shard_range(n: int, rank: int, world: int):
     lo = (n * rank) // world
     hi = (n * (rank + 1)) // world
     return lo, hi
+
+
+# ----------------------------------------------------------- NEXT rows (§8(f))
+CORR_TERMS = 1024          # P:494 "1024 Terms and 16384 Documents"
+CORR_DOCS = 16384
+SPMV_N = 44609             # P:487 bcsstk32: 44609 x 44609, 1029655 non-zeros
+SPMV_NNZ = 1029655
+CONV_N = 2048              # P:489 "2048 x 2048 image with a 5 x 5 filter"
+
+
+def corr_bitsets(terms: int = CORR_TERMS, docs: int = CORR_DOCS, density: float = 0.5, seed: int = 1006):
+    """(terms, docs/32) uint32: bit d%32 of word d/32 = document d contains the term."""
+    assert docs % 32 == 0
+    bits = rng(seed).random((terms, docs)) < density
+    packed = np.packbits(bits.reshape(terms, docs // 8, 8), axis=-1, bitorder="little")
+    return np.ascontiguousarray(packed.reshape(terms, docs // 8)).view(np.uint32).reshape(terms, docs // 32)
+
+
+def banded_csr(n: int = SPMV_N, nnz: int = SPMV_NNZ, bandwidth: int = 1600, seed: int = 1007):
+    """Synthetic stand-in for bcsstk32 (no dataset offline): n x n, ~nnz
+    non-zeros, symmetric pattern inside a band, every diagonal present,
+    values U[-1, 1).  Returns (row_ptr int32[n+1], col int32[nnz'], val f32[nnz'])."""
+    g = rng(seed)
+    per_row = max(0, (nnz - n) // (2 * n))          # off-diagonal pairs per row
+    i = np.repeat(np.arange(n), per_row)
+    j = i + g.integers(1, bandwidth, i.size)
+    keep = j < n
+    i, j = i[keep], j[keep]
+    rows = np.concatenate([np.arange(n), i, j])
+    cols = np.concatenate([np.arange(n), j, i])
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = (key // n).astype(np.int32), (key % n).astype(np.int32)
+    row_ptr = np.zeros(n + 1, np.int32)
+    np.add.at(row_ptr, rows + 1, 1)
+    row_ptr = np.cumsum(row_ptr, dtype=np.int64).astype(np.int32)
+    val = (g.random(cols.size, dtype=np.float32) * 2 - 1).astype(np.float32)
+    return row_ptr, cols, val

@@ -1,0 +1,76 @@
+"""GPU parity for the SURVEY §8(f) NEXT rows, through the C-ABI."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+J = pytest.importorskip("paper_1508_06791_b200")
+from paper_1508_06791_b200 import jacc  # noqa: E402
+from paper_1508_06791_b200.torch_glue import make_graph  # noqa: E402
+
+R, W = J.JACC_READ, J.JACC_WRITE
+
+
+def _conv(img, f):
+    H, Wd = img.shape
+    k = f.shape[0]
+    out = np.zeros_like(img)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(out, W)],
+               jacc.jacc_conv2d_params_t(H, Wd, k // 2, 0))
+    g.run()
+    g.destroy()
+    return out
+
+
+@pytest.mark.parametrize("H,Wd,r", [(1, 1, 2), (7, 9, 2), (33, 65, 1), (256, 256, 2), (100, 37, 3),
+                                    (64, 64, 4), (2048, 2048, 2)])
+def test_conv2d_tolerance(H, Wd, r):
+    img = synth.uniform_f32(H * Wd, 100 + H, -1, 1).reshape(H, Wd)
+    f = synth.uniform_f32((2 * r + 1) ** 2, 200 + r, -1, 1).reshape(2 * r + 1, 2 * r + 1)
+    out = _conv(img, f)
+    ref, ab = oracle.conv2d(img, f)
+    # map: 1e-5 of the output's natural scale sum |f| |img|
+    assert np.all(np.abs(out - ref) <= 1e-5 * ab + 1e-30)
+
+
+@pytest.mark.parametrize("ta,tb,docs", [(1, 1, 32), (5, 7, 96), (100, 70, 1000 * 32 // 32 * 32),
+                                        (1024, 1024, 16384)])
+def test_corr_bit_exact(ta, tb, docs):
+    A = synth.corr_bitsets(ta, docs, 0.5, seed=ta)
+    B = synth.corr_bitsets(tb, docs, 0.3, seed=tb + 1)
+    C = np.zeros((ta, tb), np.int32)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(A.view(np.int32), R), g.a(B.view(np.int32), R), g.a(C, W)],
+               jacc.jacc_corr_params_t(ta, tb, docs // 32))
+    g.run()
+    g.destroy()
+    assert np.array_equal(C, oracle.corr_popc(A, B))
+
+
+@pytest.mark.parametrize("n,nnz,bw", [(1, 1, 1), (100, 900, 10), (5000, 100000, 300),
+                                      (synth.SPMV_N, synth.SPMV_NNZ, 1600)])
+def test_spmv_tolerance(n, nnz, bw):
+    rp, col, val = synth.banded_csr(n, nnz, bandwidth=bw, seed=n)
+    x = synth.uniform_f32(n, 5, -1, 1)
+    y = np.zeros(n, np.float32)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(rp, R), g.a(col, R), g.a(val, R), g.a(x, R), g.a(y, W)],
+               jacc.jacc_spmv_params_t(n, n))
+    g.run()
+    g.destroy()
+    ref, ab = oracle.spmv_csr(rp, col, val, x)
+    assert np.all(np.abs(y - ref) <= 1e-5 * ab + 1e-30)
+
+
+def test_conv2d_delta_exact():
+    f = synth.uniform_f32(25, 3).reshape(5, 5)
+    img = np.zeros((40, 50), np.float32)
+    img[0, 0] = 1.0; img[20, 30] = 1.0; img[39, 49] = 1.0
+    out = _conv(img, f)
+    ref, _ = oracle.conv2d(img, f)
+    assert np.array_equal(out.astype(np.float64), ref)
