@@ -46,9 +46,9 @@ inline void pick_grid(const jacc_schedule_t *s, int64_t work_blocks, int per_sm,
                       int *block) {
     int b = def_block;
     int64_t gsz;
-    if (s && s->group[0] > 0) {
+    if (s && s->group[0] > 0) {   // def_block is also the kernel's __launch_bounds__
         b = s->group[0];
-        if (b > 1024) b = 1024;
+        if (b > def_block) b = def_block;
         b = (b + 31) / 32 * 32;
     }
     if (s && s->global[0] > 0) {

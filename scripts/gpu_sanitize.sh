@@ -1,0 +1,36 @@
+# compute-sanitizer (memcheck / racecheck / synccheck) over small graphs of every op
+set -x
+cat > /tmp/san.py <<'PY'
+import numpy as np, sys
+sys.path.insert(0, ".")
+import synth
+import paper_1508_06791_b200 as J
+from paper_1508_06791_b200 import jacc
+R, W, RW = 1, 2, 3
+g = J.Graph()
+n = 20011
+a, b = synth.vadd_inputs(n); c = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
+keys = synth.hist_keys(n + 3); bins = np.zeros(256, np.int32); big = np.zeros(1000, np.int32)
+u = synth.bs_rand(n); call = np.zeros(n, np.float32); put = np.zeros(n, np.float32)
+A, B = synth.sgemm_inputs(200, 300, 100, "signed"); C = np.zeros((200, 300), np.float32)
+pos, vel = synth.nbody_state(700); pos2 = np.zeros_like(pos)
+img = synth.uniform_f32(100 * 77, 1).reshape(100, 77); f = synth.uniform_f32(25, 2).reshape(5, 5); out = np.zeros_like(img)
+bits = synth.corr_bitsets(70, 320); cc = np.zeros((70, 70), np.int32)
+rp, col, val = synth.banded_csr(500, 5000, 30); x = synth.uniform_f32(500, 3); y = np.zeros(500, np.float32)
+g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins, W)], jacc.jacc_hist_params_t(256))
+g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(big, W)], jacc.jacc_hist_params_t(1000))
+g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(u, R), g.a(call, W), g.a(put, W)])
+g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A, R), g.a(B, R), g.a(C, W)], jacc.jacc_sgemm_params_t(200, 300, 100, 100, 300, 300, 0, 0))
+g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(pos, R, f32x4=True), g.a(vel, RW, f32x4=True), g.a(pos2, W, f32x4=True)], jacc.jacc_nbody_params_t(0, 0.016, 0.01, 1.0))
+g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(out, W)], jacc.jacc_conv2d_params_t(100, 77, 2, 0))
+g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits.view(np.int32), R), g.a(bits.view(np.int32), R), g.a(cc, W)], jacc.jacc_corr_params_t(70, 70, 10))
+g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(rp, R), g.a(col, R), g.a(val, R), g.a(x, R), g.a(y, W)], jacc.jacc_spmv_params_t(500, 500))
+g.run(); g.run()
+print("ok", g.stats()["launches"])
+g.destroy()
+PY
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san.py > gpurun_out/san_$tool.txt 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/san_$tool.txt
+done

@@ -67,6 +67,30 @@ def test_vadd_unaligned_device_args(off):
     g.destroy()
 
 
+@pytest.mark.parametrize("glob,group", [(32, 32), (1000, 64), (1 << 14, 128), (1 << 22, 1024), (0, 96)])
+def test_schedule_invariance(glob, group):
+    """R15 / P:162-165: the launch schedule (threads, group size) is advisory --
+    fewer threads than iterations is a block-cyclic mapping -- and never
+    changes a result: maps and the histogram are bitwise identical."""
+    n = 300007
+    a, b = synth.vadd_inputs(n, seed=5)
+    keys = synth.hist_keys(n, seed=6)
+    u = synth.bs_rand(n, seed=7)
+    outs = []
+    for sched in (None, jacc.jacc_schedule_t((glob, 0, 0), (group, 0, 0), 0)):
+        c = np.zeros(n, np.float32); bins = np.zeros(256, np.int32)
+        call = np.zeros(n, np.float32); put = np.zeros(n, np.float32)
+        g = _graph()
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)], sched=sched)
+        g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins, W)], jacc.jacc_hist_params_t(256), sched=sched)
+        g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(u, R), g.a(call, W), g.a(put, W)], sched=sched)
+        g.run()
+        g.destroy()
+        outs.append((c, bins, call, put))
+    for x, y in zip(outs[0], outs[1]):
+        assert np.array_equal(x, y)
+
+
 # ---------------------------------------------------------------- reduce
 @pytest.mark.parametrize("n", [0, 1, 7, 4097, 1 << 20, (1 << 25) + 5])
 def test_reduce_tolerance(n):
