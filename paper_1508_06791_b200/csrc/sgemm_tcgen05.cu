@@ -37,11 +37,15 @@
 namespace jacc_k {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 32;      // BK * 4 B = one 128-byte swizzle row
-constexpr int kStages = 2;
-constexpr int kABytes = BM * BK * 4;            // 16 KB
-constexpr int kBBytes = BN * BK * 4;            // 32 KB
-constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;   // 96 KB
+// Swizzle width of the K-major smem tiles: one swizzle row = kSw bytes = BK
+// tf32.  64 B rows give 48 KB stages, so 4 stages fit (128 B rows: 96 KB,
+// only 2 stages -- the TMA latency then shows up as MMA bubbles).
+constexpr int kSw = 64;
+constexpr int BM = 128, BN = 256, BK = kSw / 4;
+constexpr int kStages = kSw == 64 ? 4 : 2;
+constexpr int kABytes = BM * BK * 4;
+constexpr int kBBytes = BN * BK * 4;
+constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;   // 48 KB (kSw 64) / 96 KB (kSw 128)
 constexpr int kThreads = 320;                   // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kTmemCols = 512;                  // two 128 x 256 fp32 accumulators
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
@@ -85,9 +89,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     uint64_t d = 0;
     d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address  [0,14)
     d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major) [16,30)
-    d |= (uint64_t)(1024 >> 4) << 32;                // SBO = 1024 B   [32,46)
+    d |= (uint64_t)((8 * kSw) >> 4) << 32;          // SBO = 8 rows x kSw B  [32,46)
     d |= (uint64_t)1 << 46;                          // version = 1 (sm_100)
-    d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
+    d |= (uint64_t)(kSw == 64 ? 4 : 2) << 61;        // layout: SWIZZLE_64B / SWIZZLE_128B
     return d;
 }
 // Instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, M=128, N=256.
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(256) split_bt_kernel(const float *__restrict__
 // registers with round-to-nearest adds while the MMAs fill the other buffer
 // (the FP8 "promotion" pattern, here for TF32).  Bias per chunk ~ 96
 // truncated adds ~ 5e-6 relative.
-constexpr int kChunkKB = 8;
+constexpr int kChunkKB = 256 / BK;
 constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quarter, 128 columns each
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -334,7 +338,8 @@ bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int b
     cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, kSw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -365,7 +370,7 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
     {
         dim3 g1((unsigned)((Kp + 1023) / 1024), (unsigned)(Mp < 65535 ? Mp : 65535));
         split_a_kernel<<<g1, 256, 0, st>>>(A, M, K, p->lda, ahi, alo, Mp, Kp);
-        dim3 g2((unsigned)(Np / 32), (unsigned)(Kp / 32));
+        dim3 g2((unsigned)(Np / 32), (unsigned)((Kp + 31) / 32));
         split_bt_kernel<<<g2, 256, 0, st>>>(B, K, N, p->ldb, bhi, blo, Np, Kp);
         *launches += 2;
     }
