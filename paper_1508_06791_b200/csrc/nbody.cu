@@ -49,8 +49,8 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // (FADD2/FFMA2/FMUL2, FMA-heavy pipe) -- half the FP32 issue slots of scalar
 // code for the same arithmetic: per pair and source 12 paired ops + 2
 // MUFU.RSQ.  Target k of thread tid is t0 + tid + k * kBlock.
-template <int P>
-__global__ void __launch_bounds__(kBlock) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
+template <int P, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
     constexpr int T = 2 * P;
@@ -149,7 +149,12 @@ Variant variant() {
         // at 2^17 bodies).  JACC_NBODY_PAIRS overrides it for experiments.
         const char *e = getenv("JACC_NBODY_PAIRS");
         const int P = e ? atoi(e) : 4;
-        v = P == 2 ? Variant{nbody_partial_kernel<2>, 4} : Variant{nbody_partial_kernel<4>, 8};
+        const char *m = getenv("JACC_NBODY_MINB");
+        const int MB = m ? atoi(m) : 1;
+#define V(p, mb) if (P == p && MB == mb) v = Variant{nbody_partial_kernel<p, mb>, 2 * p}
+        V(2, 1); V(4, 1); V(3, 1); V(4, 10); V(3, 12); V(5, 1); V(4, 8);
+#undef V
+        if (!v.fn) v = Variant{nbody_partial_kernel<4, 1>, 8};
     }
     return v;
 }
