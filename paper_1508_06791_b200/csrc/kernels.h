@@ -50,8 +50,9 @@ cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt
                        cudaStream_t st, int *launches);
 
 // correlation matrix
+size_t corr_ws_bytes(int64_t ta, int64_t tb, int64_t words);
 cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int64_t tb, int64_t words, int32_t *C,
-                          cudaStream_t st, int *launches);
+                          void *ws, cudaStream_t st, int *launches);
 
 // SpMV CSR
 cudaError_t spmv_csr_f32(const int32_t *row_ptr, const int32_t *col, const float *val, const float *x, float *y,

@@ -6,15 +6,15 @@
 // tgt_offset .. tgt_offset + n_tgt - 1 (a rank's shard in SPMD, R17).
 //
 // sm_100a design (FP32-pipe bound: 12 fp32 ops + 1 MUFU.RSQ per interaction):
-//   * work unit = (64 threads x 8 targets) x (one chunk of kChunk = 8192
+//   * work unit = (64 threads x 6 targets) x (one chunk of kChunk = 8192
 //     sources); the chunk size depends on nothing but the source count, so
 //     every rank of a sharded run sums a target's sources in exactly the same
 //     groups as one GPU does (bitwise shard invariance, §8(e)), and 2^17
-//     bodies give 4096 units -- 27.7 per SM, the 148 SMs finish together;
+//     bodies give ~5.5k units -- 37 per SM, the 148 SMs finish together;
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
 //     pairs of the paired FP32 instructions;
-//   * each thread holds 4 target PAIRS in registers and uses the sm_100
+//   * each thread holds 3 target PAIRS in registers and uses the sm_100
 //     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops + 2 MUFU.RSQ per
 //     pair and source, half the FP32 issue slots of scalar code;
 //     measured alternatives (scalar FP32 on the other pipe for some targets,
@@ -24,9 +24,6 @@
 //     adds the chunks in order and applies kick + drift;
 //   * the self term is included: x_j - x_i = 0 with eps2 > 0 contributes 0;
 //     padding sources (j >= n_src) have m = 0 at the origin (contribute 0).
-#include <cstdio>
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -49,7 +46,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // (FADD2/FFMA2/FMUL2, FMA-heavy pipe) -- half the FP32 issue slots of scalar
 // code for the same arithmetic: per pair and source 12 paired ops + 2
 // MUFU.RSQ.  Target k of thread tid is t0 + tid + k * kBlock.
-template <int P, int MINB>
+template <int P, int MINB, int UNR>
 __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
@@ -85,7 +82,7 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float
         float2 tx[P], ty[P], tz[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = f2(0.f, 0.f);
-#pragma unroll 4
+#pragma unroll UNR
         for (int s = 0; s < kTile; ++s) {
             const float4 A = tile[TW * s], B = tile[TW * s + 1];
             const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
@@ -142,22 +139,9 @@ __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restr
 typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
 struct Variant { partial_fn fn; int tpt; };
 
-Variant variant() {
-    static Variant v = {nullptr, 0};
-    if (!v.fn) {
-        // pairs per thread; 4 measured best on B200 (6.83 ms vs 6.94 ms for 2
-        // at 2^17 bodies).  JACC_NBODY_PAIRS overrides it for experiments.
-        const char *e = getenv("JACC_NBODY_PAIRS");
-        const int P = e ? atoi(e) : 4;
-        const char *m = getenv("JACC_NBODY_MINB");
-        const int MB = m ? atoi(m) : 1;
-#define V(p, mb) if (P == p && MB == mb) v = Variant{nbody_partial_kernel<p, mb>, 2 * p}
-        V(2, 1); V(4, 1); V(3, 1); V(4, 10); V(3, 12); V(5, 1); V(4, 8);
-#undef V
-        if (!v.fn) v = Variant{nbody_partial_kernel<4, 1>, 8};
-    }
-    return v;
-}
+// 3 target pairs per thread, source loop unrolled by 4: measured best on B200
+// at 2^17 bodies (ms/step: P=3 6.70, P=2 6.75, P=4 7.01; unroll 2/8 slower).
+Variant variant() { return Variant{nbody_partial_kernel<3, 1, 4>, 6}; }
 
 }  // namespace
 

@@ -610,6 +610,11 @@ int prepare_memory(jacc_graph *g) {
                 break;
             case JACC_OP_SGEMM_F32: need = jacc_k::sgemm_ws_bytes((const jacc_sgemm_params_t *)T.params.data()); break;
             case JACC_OP_NBODY_STEP_F32: need = jacc_k::nbody_ws_bytes((int64_t)a[0].count, (int64_t)a[1].count); break;
+            case JACC_OP_CORR_POPC_U32: {
+                const jacc_corr_params_t *cp = (const jacc_corr_params_t *)T.params.data();
+                need = jacc_k::corr_ws_bytes(cp->ta, cp->tb, cp->words);
+                break;
+            }
             default: break;
         }
         if (need > T.ws_bytes) {
@@ -677,7 +682,7 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
         case JACC_OP_CORR_POPC_U32: {
             const jacc_corr_params_t *cp = (const jacc_corr_params_t *)T.params.data();
             e = jacc_k::corr_popc_u32((const uint32_t *)P(0), cp->ta, (const uint32_t *)P(1), cp->tb, cp->words,
-                                      (int32_t *)P(2), st, launches);
+                                      (int32_t *)P(2), T.ws, st, launches);
             break;
         }
         case JACC_OP_SPMV_CSR_F32:

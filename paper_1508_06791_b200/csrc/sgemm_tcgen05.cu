@@ -33,6 +33,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace jacc_k {
 namespace {
@@ -52,48 +53,17 @@ constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrie
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// ------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// ------------------------------------------------------------ PTX wrappers (tcgen05.cuh)
+using tc::mbar_expect_tx;
+using tc::mbar_init;
+using tc::mbar_wait;
+using tc::smem_u32;
+using tc::tma_load_2d;
+using tc::tma_prefetch;
+__device__ __forceinline__ void tc_fence_before() { tc::fence_before(); }
+__device__ __forceinline__ void tc_fence_after() { tc::fence_after(); }
 
-// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address  [0,14)
-    d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major) [16,30)
-    d |= (uint64_t)((8 * kSw) >> 4) << 32;          // SBO = 8 rows x kSw B  [32,46)
-    d |= (uint64_t)1 << 46;                          // version = 1 (sm_100)
-    d |= (uint64_t)(kSw == 64 ? 4 : 2) << 61;        // layout: SWIZZLE_64B / SWIZZLE_128B
-    return d;
-}
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) { return tc::desc_kmajor(addr, kSw); }
 // Instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, M=128, N=256.
 constexpr uint32_t kIdesc = (1u << 4)                // c_format = F32
                             | (2u << 7)              // a_format = TF32
@@ -107,21 +77,8 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(kIdesc), "r"(accum));
 }
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-
-#define TMEM_LD_32(taddr, r)                                                                                   \
-    asm volatile(                                                                                              \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
-        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                     \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),           \
-          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),           \
-          "=r"(r[30]), "=r"(r[31])                                                                             \
-        : "r"(taddr))
+__device__ __forceinline__ void mma_commit(uint32_t bar) { tc::commit(bar); }
+#define TMEM_LD_32(taddr, r) JACC_TMEM_LD_32(taddr, r)
 
 // ------------------------------------------------------------ split kernels
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -145,25 +102,44 @@ __global__ void __launch_bounds__(256) split_a_kernel(const float *__restrict__ 
 }
 
 // B (K x N, row stride ldb) -> hi/lo of B^T, [Np x Kp] row-major (K contiguous).
+// 64 (k) x 64 (n) tile per 256-thread block through shared memory: each
+// thread reads 4 x 16 B along n (rows of B) and writes 4 x 16 B along k (rows
+// of B^T) for hi and for lo -- 128-bit accesses on both sides.
 __global__ void __launch_bounds__(256) split_bt_kernel(const float *__restrict__ B, int64_t K, int64_t N, int64_t ldb,
                                                        float *__restrict__ hi, float *__restrict__ lo, int64_t Np,
                                                        int64_t Kp) {
-    __shared__ float t[32][33];
-    const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
-    for (int j = ty; j < 32; j += 8) {
-        const int64_t k = k0 + j, n = n0 + tx;
-        t[j][tx] = (k < K && n < N) ? B[k * ldb + n] : 0.f;
+    __shared__ float t[64][65];
+    const int64_t k0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+    const bool vec_in = ((ldb & 3) == 0) && (((uintptr_t)B & 15) == 0) && n0 + 64 <= N && k0 + 64 <= K;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int q = threadIdx.x + 256 * i;        // 1024 float4 of the 64 x 64 tile
+        const int r = q >> 4, c4 = (q & 15) * 4;    // k row, n column
+        const int64_t k = k0 + r;
+        if (vec_in) {
+            const float4 v = *(const float4 *)(B + k * ldb + n0 + c4);
+            t[r][c4] = v.x; t[r][c4 + 1] = v.y; t[r][c4 + 2] = v.z; t[r][c4 + 3] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t n = n0 + c4 + j;
+                t[r][c4 + j] = (k < K && n < N) ? B[k * ldb + n] : 0.f;
+            }
+        }
     }
     __syncthreads();
-    for (int j = ty; j < 32; j += 8) {
-        const int64_t n = n0 + j, k = k0 + tx;
-        if (n < Np && k < Kp) {
-            const float x = t[tx][j];
-            const float h = tf32_hi(x);
-            hi[n * Kp + k] = h;
-            lo[n * Kp + k] = x - h;
-        }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int q = threadIdx.x + 256 * i;
+        const int r = q >> 4, c4 = (q & 15) * 4;    // n row of B^T, k column
+        const int64_t n = n0 + r, k = k0 + c4;
+        if (n >= Np || k >= Kp) continue;           // Kp is a multiple of 16: k..k+3 < Kp
+        float4 h, l;
+        const float x0 = t[c4][r], x1 = t[c4 + 1][r], x2 = t[c4 + 2][r], x3 = t[c4 + 3][r];
+        h.x = tf32_hi(x0); h.y = tf32_hi(x1); h.z = tf32_hi(x2); h.w = tf32_hi(x3);
+        l.x = x0 - h.x; l.y = x1 - h.y; l.z = x2 - h.z; l.w = x3 - h.w;
+        *(float4 *)(hi + n * Kp + k) = h;
+        *(float4 *)(lo + n * Kp + k) = l;
     }
 }
 
@@ -212,12 +188,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(tfull0 + 8 * b, 1);
             mbar_init(tempty0 + 8 * b, kEpiWarps);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tc::fence_barrier_init();
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tc::alloc_cols(smem_u32(tmem_slot), kTmemCols);
     }
     tc_fence_before();
     __syncthreads();
@@ -282,13 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 4; ++j) {
                 uint32_t r[32];
                 TMEM_LD_32(taddr + j * 32, r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                tc::wait_ld();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[j * 32 + i] += __uint_as_float(r[i]);
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * buf) : "memory");
+            if (lane == 0) tc::mbar_arrive(tempty0 + 8 * buf);
         }
         const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
         if (row < M) {
@@ -309,38 +283,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+        tc::dealloc_cols(tmem_base, kTmemCols);
     }
 }
 
 // ------------------------------------------------------------ host side
-typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-encode_fn_t get_encode() {
-    static encode_fn_t fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (encode_fn_t)p;
-    }
-    return fn;
-}
-
 bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int box_rows) {
-    encode_fn_t enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
-    cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
-    cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, kSw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return tc::make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, kp, kp * 4, box_rows, BK, kSw);
 }
 
 }  // namespace
@@ -370,7 +319,7 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
     {
         dim3 g1((unsigned)((Kp + 1023) / 1024), (unsigned)(Mp < 65535 ? Mp : 65535));
         split_a_kernel<<<g1, 256, 0, st>>>(A, M, K, p->lda, ahi, alo, Mp, Kp);
-        dim3 g2((unsigned)(Np / 32), (unsigned)((Kp + 31) / 32));
+        dim3 g2((unsigned)((Np + 63) / 64), (unsigned)((Kp + 63) / 64));
         split_bt_kernel<<<g2, 256, 0, st>>>(B, K, N, p->ldb, bhi, blo, Np, Kp);
         *launches += 2;
     }
