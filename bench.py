@@ -346,9 +346,10 @@ def cfg1_latency(torch, J, reps=200):
     R, W = J.JACC_READ, J.JACC_WRITE
     a, b = synth.vadd_inputs()
     out = {}
-    for mode in ("direct", "replay", "e2e_direct", "e2e_replay"):
+    modes = {"direct": 0, "replay": J.JACC_GRAPH_REPLAY, "merge_replay": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY,
+             "e2e_direct": 0, "e2e_merge": J.JACC_GRAPH_MERGE}
+    for mode, flags in modes.items():
         host = mode.startswith("e2e")
-        flags = J.JACC_GRAPH_REPLAY if mode.endswith("replay") else 0
         g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=flags)
         if host:
             ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()

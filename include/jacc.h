@@ -97,6 +97,14 @@ typedef enum jacc_dtype {
                                 (e.g. pageable host memory) is issued
                                 directly; stats.graph_captures/replays say
                                 which happened                              */
+#define JACC_GRAPH_MERGE 8u  /* task merge ("eliminate, merge and
+                                re-organize"): a vadd task
+                                immediately followed by a reduce task of its
+                                output on the same stream is issued as ONE
+                                fused kernel (c written, its sum taken in the
+                                same pass, bit-identical to the pair); the
+                                action list and counted copies are unchanged,
+                                both tasks report the fused kernel's time   */
 
 /* -------------------------------------------------------------- ops */
 typedef enum jacc_op {

@@ -21,6 +21,10 @@ cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,
 size_t reduce_ws_bytes(int64_t n);
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws,
                            const jacc_schedule_t *s, cudaStream_t st, int *launches);
+// the runtime's "merge" of vadd -> reduce: c = a + b, out[0] += sum(c)
+bool vadd_reduce_fusable(const float *a, const float *b, const float *c);
+cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n, float *out, void *ws,
+                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches);
 
 // bins[k] += #{keys == k}
 size_t histogram_ws_bytes(int64_t n, int nbins);

@@ -33,7 +33,13 @@ __device__ __forceinline__ float block_sum(float v, float *sh) {
     return v;   // valid in thread 0
 }
 
-__global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, int64_t n, int64_t head,
+// kFused (the runtime's "merge" of vadd -> reduce): the element
+// value is a[i] + b[i] (one fp32 add, exactly the vadd kernel's), stored to
+// c and summed in the very same order as reduce_kernel<false> on c -- so the
+// merged pair produces bit-identical c and s in one pass over a and b.
+template <bool kFused>
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, const float *__restrict__ xb,
+                                                        float *__restrict__ xc, int64_t n, int64_t head,
                                                         float *__restrict__ out, float *__restrict__ partials,
                                                         unsigned *__restrict__ ticket) {
     __shared__ float sh[32];
@@ -42,21 +48,35 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     // unaligned head (< 4 scalars), then 128-bit body, then tail (< 4 scalars)
-    if (tid < head) a0 += x[tid];
-    const float4 *x4 = (const float4 *)(x + head);
+    auto elem = [&](int64_t j) -> float {
+        if (!kFused) return x[j];
+        const float v = x[j] + xb[j];
+        xc[j] = v;
+        return v;
+    };
+    auto vec = [&](int64_t j) -> float4 {   // j indexes float4 from x + head
+        float4 u = ld_stream((const float4 *)(x + head) + j);
+        if (kFused) {
+            const float4 w = ld_stream((const float4 *)(xb + head) + j);
+            u = make_float4(u.x + w.x, u.y + w.y, u.z + w.z, u.w + w.w);
+            st_stream((float4 *)(xc + head) + j, u);
+        }
+        return u;
+    };
+    if (tid < head) a0 += elem(tid);
     const int64_t n4 = (n - head) / 4;
     int64_t i = tid;
     for (; i + stride < n4; i += 2 * stride) {
-        float4 u = ld_stream(x4 + i), v = ld_stream(x4 + i + stride);
+        float4 u = vec(i), v = vec(i + stride);
         a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
         a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
     }
     if (i < n4) {
-        float4 u = ld_stream(x4 + i);
+        float4 u = vec(i);
         a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
     }
     const int64_t t0 = head + 4 * n4;
-    if (tid < n - t0) a1 += x[t0 + tid];
+    if (tid < n - t0) a1 += elem(t0 + tid);
     float s = block_sum((a0 + a1) + (a2 + a3), sh);
     if (threadIdx.x == 0) {
         partials[blockIdx.x] = s;
@@ -79,18 +99,40 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
 
 size_t reduce_ws_bytes(int64_t) { return sizeof(float) * kMaxGrid + 128; }
 
+namespace {
+void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
+    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, grid, block);
+    *block = kBlock;   // the block tree assumes kBlock threads
+    if (*grid > kMaxGrid) *grid = kMaxGrid;
+}
+}  // namespace
+
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, const jacc_schedule_t *s,
                            cudaStream_t st, int *launches) {
     int grid, block;
     const int64_t head = (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4) < n
                              ? (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4)
                              : n;
-    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, &grid, &block);
-    block = kBlock;   // the block tree assumes kBlock threads
-    if (grid > kMaxGrid) grid = kMaxGrid;
+    reduce_grid(n, s, &grid, &block);
     float *partials = (float *)ws;
     unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
-    reduce_kernel<<<grid, block, 0, st>>>(x, n, head, out, partials, ticket);
+    reduce_kernel<false><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+bool vadd_reduce_fusable(const float *a, const float *b, const float *c) {
+    return aligned16(a) && aligned16(b) && aligned16(c);
+}
+
+// c = a + b and out[0] += sum(c) in one pass (requires vadd_reduce_fusable).
+cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n, float *out, void *ws,
+                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches) {
+    int grid, block;
+    reduce_grid(n, s_reduce, &grid, &block);
+    float *partials = (float *)ws;
+    unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
+    reduce_kernel<true><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket);
     ++*launches;
     return cudaGetLastError();
 }

@@ -721,6 +721,20 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
     return JACC_OK;
 }
 
+// JACC_GRAPH_MERGE ("merge"): task i = vadd whose output c is the input
+// of task i + 1 = reduce, on the same stream, pointers 16-byte aligned ->
+// index of the reduce task to fuse with it, else -1.
+int merge_partner(const jacc_graph *g, int i) {
+    if (!(g->cfg.flags & JACC_GRAPH_MERGE) || (g->cfg.flags & JACC_GRAPH_NAIVE) || g->cfg.fail_task > 0) return -1;
+    const int j = i + 1;
+    if (j >= (int)g->tasks.size()) return -1;
+    const Task &V = g->tasks[i], &R = g->tasks[j];
+    if (V.op != JACC_OP_VADD_F32 || R.op != JACC_OP_REDUCE_SUM_F32) return -1;
+    if (R.args[0].buf != V.args[2].buf || R.stream != V.stream) return -1;
+    auto P = [&](const Task &U, int k) { return (const float *)g->bufs[U.args[k].buf].dptr; };
+    return jacc_k::vadd_reduce_fusable(P(V, 0), P(V, 1), P(V, 2)) ? j : -1;
+}
+
 int issue(jacc_graph *g) {
     const int nb = (int)g->bufs.size();
     std::vector<char> h2d_issued(nb, 0);
@@ -745,33 +759,52 @@ int issue(jacc_graph *g) {
             CK(cudaEventRecord(B.ev_h2d, g->h2d));
             h2d_issued[A.buf] = 1;
         } else if (A.kind == A_KERNEL || A.kind == A_COLLECTIVE) {
+            if (task_done[A.task]) continue;   // issued inside an earlier merged kernel
             Task &T = g->tasks[A.task];
             if (g->cfg.fail_task > 0 && A.task == g->cfg.fail_task - 1)
                 return fail(JACC_ERR_INJECTED, "failure injected at task %d", A.task);
             cudaStream_t st = stream_of(g, T);
-            for (const TaskArg &a : T.args)
-                if (h2d_issued[a.buf] && g->h2d != st) CK(cudaStreamWaitEvent(st, g->bufs[a.buf].ev_h2d, 0));
-            for (int p : T.preds) {
-                const Task &Pt = g->tasks[p];
-                if (stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_dep, 0));
-            }
+            const int partner = merge_partner(g, A.task);   // -1, or the reduce task fused with it
             // timing events: under CUDA-graph capture they must be EXTERNAL
             // record nodes (a plain record is only a capture dependency)
-            CK(g->capturing ? cudaEventRecordWithFlags(T.ev_start, st, cudaEventRecordExternal)
-                            : cudaEventRecord(T.ev_start, st));
-            // MEMSET0 actions of this task (auto-zero of @Atomic outputs)
-            for (size_t bj = ai; bj-- > 0;) {
-                const Action &M = g->plan[bj];
-                if (M.kind != A_MEMSET0) break;
-                if (M.task == A.task)
-                    CK(cudaMemsetAsync(g->bufs[M.buf].dptr, 0, g->bufs[M.buf].bytes, st));
+            auto rec = [&](cudaEvent_t e) {
+                return g->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+            };
+            for (int t : {A.task, partner}) {
+                if (t < 0) continue;
+                const Task &U = g->tasks[t];
+                for (const TaskArg &a : U.args)
+                    if (h2d_issued[a.buf] && g->h2d != st) CK(cudaStreamWaitEvent(st, g->bufs[a.buf].ev_h2d, 0));
+                for (int p : U.preds) {
+                    const Task &Pt = g->tasks[p];
+                    if (p != A.task && stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_dep, 0));
+                }
             }
-            int rc = launch_task(g, T, st, &launches);
+            CK(rec(T.ev_start));
+            if (partner >= 0) CK(rec(g->tasks[partner].ev_start));
+            // MEMSET0 actions (auto-zero of @Atomic outputs) of this task
+            // and of a merged partner (they sit just before its KERNEL action)
+            for (const Action &M : g->plan)
+                if (M.kind == A_MEMSET0 && (M.task == A.task || M.task == partner))
+                    CK(cudaMemsetAsync(g->bufs[M.buf].dptr, 0, g->bufs[M.buf].bytes, st));
+            int rc;
+            if (partner >= 0) {
+                const Task &Rt = g->tasks[partner];
+                auto P = [&](const Task &U, int i) { return g->bufs[U.args[i].buf].dptr; };
+                cudaError_t e = jacc_k::vadd_reduce_f32(
+                    (const float *)P(T, 0), (const float *)P(T, 1), (float *)P(T, 2), (int64_t)T.args[0].count,
+                    (float *)P(Rt, 1), Rt.ws, Rt.has_sched ? &Rt.sched : nullptr, st, &launches);
+                rc = e == cudaSuccess ? JACC_OK : fail(JACC_ERR_CUDA, "launch vadd+reduce: %s", cudaGetErrorString(e));
+            } else {
+                rc = launch_task(g, T, st, &launches);
+            }
             if (rc != JACC_OK) return rc;
-            CK(g->capturing ? cudaEventRecordWithFlags(T.ev_end, st, cudaEventRecordExternal)
-                            : cudaEventRecord(T.ev_end, st));
-            CK(cudaEventRecord(T.ev_dep, st));   // cross-stream dependency marker
-            task_done[A.task] = 1;
+            for (int t : {A.task, partner}) {
+                if (t < 0) continue;
+                CK(rec(g->tasks[t].ev_end));
+                CK(cudaEventRecord(g->tasks[t].ev_dep, st));   // cross-stream dependency marker
+                task_done[t] = 1;
+            }
         } else if (A.kind == A_D2H) {
             Buffer &B = g->bufs[A.buf];
             const Task &W = g->tasks[A.task];

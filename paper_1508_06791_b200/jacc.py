@@ -31,7 +31,7 @@ JACC_OK, JACC_ERR_INVALID_ARG, JACC_ERR_STATE, JACC_ERR_ACCESS, JACC_ERR_ALIAS, 
 JACC_F32, JACC_I32, JACC_F32X4 = 1, 2, 3
 JACC_READ, JACC_WRITE, JACC_READWRITE = 1, 2, 3
 JACC_ARG_DEVICE, JACC_ARG_CACHABLE = 1, 2
-JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY = 1, 2, 4
+JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY, JACC_GRAPH_MERGE = 1, 2, 4, 8
 JACC_MAX_STREAMS = 8
 (JACC_OP_VADD_F32, JACC_OP_REDUCE_SUM_F32, JACC_OP_HISTOGRAM_I32, JACC_OP_BLACKSCHOLES_F32,
  JACC_OP_BLACKSCHOLES_SOA_F32, JACC_OP_SGEMM_F32, JACC_OP_NBODY_STEP_F32, JACC_OP_ALLREDUCE_SUM,

@@ -212,3 +212,28 @@ def test_plan_replay_pageable_falls_back_to_direct_issue():
         g.run()
         assert np.array_equal(c, oracle.vadd(a, b))
     g.destroy()
+
+
+@pytest.mark.parametrize("extra", [0, J.JACC_GRAPH_REPLAY])
+def test_merge_vadd_reduce_bit_identical(extra):
+    """P:289 "merge" (JACC_GRAPH_MERGE): vadd -> reduce issued as one fused
+    kernel gives bit-identical c and s, the same counted copies, one launch."""
+    n = (1 << 20) + 12
+    a, b = synth.vadd_inputs(n, seed=21)
+    outs = {}
+    for flags in (0, J.JACC_GRAPH_MERGE | extra):
+        ta = torch.from_numpy(a).pin_memory(); tb = torch.from_numpy(b).pin_memory()
+        c = torch.zeros(n).pin_memory(); s = torch.zeros(1).pin_memory()
+        g = _graph(flags=flags)
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R), g.a(tb, R), g.a(c, W)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+        for _ in range(2):
+            g.run()
+        st = g.stats()
+        outs[flags] = (c.numpy().copy(), s.numpy().copy(), st)
+        g.destroy()
+    (c0, s0, st0), (c1, s1, st1) = outs[0], outs[J.JACC_GRAPH_MERGE | extra]
+    assert np.array_equal(c0, c1) and np.array_equal(s0, s1)
+    assert np.array_equal(c0, oracle.vadd(a, b))
+    assert (st1["h2d_count"], st1["d2h_count"]) == (st0["h2d_count"], st0["d2h_count"])
+    assert st0["launches"] == 2 and st1["launches"] == 1
