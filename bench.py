@@ -337,6 +337,39 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ main arm
+def roofline_points(torch, J, peaks, reps=10):
+    """The HBM kernels of config 1 at a size where HBM, not launch latency or
+    L2, binds (2^28 elements, SURVEY §8(d) "roofline points"), L2 flushed
+    before every launch; device time from the task's CUDA events."""
+    from paper_1508_06791_b200.torch_glue import make_graph
+    R, W = J.JACC_READ, J.JACC_WRITE
+    n = 1 << 28
+    dev = torch.device("cuda", torch.cuda.current_device())
+    a = torch.rand(n, device=dev); b = torch.rand(n, device=dev)
+    c = torch.empty(n, device=dev); s = torch.zeros(1, device=dev)
+    flush = torch.empty(64 << 20, device=dev)
+    out = {}
+    for name, op, args, nbytes in (("vadd", J.JACC_OP_VADD_F32, lambda g: [g.a(a, R), g.a(b, R), g.a(c, W)], 12 * n),
+                                   ("reduce", J.JACC_OP_REDUCE_SUM_F32, lambda g: [g.a(a, R), g.a(s, W)], 4 * n)):
+        g, _ = make_graph(dev.index, n_streams=1)
+        g.add_task(op, args(g))
+        ms = []
+        for i in range(reps + 2):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            g.run()
+            if i >= 2:
+                ms.append(g.task_ms(0))
+        g.destroy()
+        m = statistics.mean(ms)
+        ach = nbytes / (m * 1e-3) / 1e9
+        out[name] = {"n": n, "ms": m, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"],
+                     "frac": ach / peaks["hbm_gbs"], "bytes_per_launch": nbytes}
+    del a, b, c, flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def cfg1_latency(torch, J, reps=200):
     """Task-graph time of BASELINE config 1 alone (vadd -> reduce, 2^20 f32):
     host wall clock per execute+sync, inputs device-resident, direct issue vs
@@ -476,6 +509,7 @@ def run_jacc(args):
     if world == 1 and not args.no_e2e:
         try:
             line["cfg1_task_graph"] = cfg1_latency(torch, J)
+            line["roofline_points_2p28"] = roofline_points(torch, J, peaks)
         except Exception as exc:   # an auxiliary measurement must not lose the bench line
             line["cfg1_task_graph"] = {"error": str(exc)[:300]}
     if not args.no_cpu_baseline and world == 1:

@@ -73,6 +73,68 @@ __device__ __forceinline__ void bs_price(float S, float K, float T, float R, flo
     put = kexp * phi_md2 - S * phi_md1;
 }
 
+// The same arithmetic on two options at once with the sm_100 paired FP32
+// instructions (FADD2 / FMUL2 / FFMA2): the FP32 work per option is
+// unchanged, its issue slots are halved -- the scalar kernel is issue-bound
+// (ncu: ~77 % issue-active with HBM at ~60 %).  MUFU ops stay per element.
+__device__ __forceinline__ float2 F2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+__device__ __forceinline__ float2 bs_poly2(float2 t) {   // t * P(t) * 0.398942280
+    constexpr double k = 0.398942280;
+    const float2 c1 = F2((float)(k * 0.319381530)), c2 = F2((float)(k * -0.356563782)),
+                 c3 = F2((float)(k * 1.781477937)), c4 = F2((float)(k * -1.821255978)),
+                 c5 = F2((float)(k * 1.330274429));
+    return mul2(t, fma2(t, fma2(t, fma2(t, fma2(t, c5, c4), c3), c2), c1));
+}
+
+__device__ __forceinline__ float2 abs2(float2 v) {   // sign bits cleared on the integer pipe (LOP3)
+    return make_float2(__uint_as_float(__float_as_uint(v.x) & 0x7fffffffu),
+                       __uint_as_float(__float_as_uint(v.y) & 0x7fffffffu));
+}
+
+// put comes from put-call parity, call - S + K e^{-RT}: an exact identity of
+// this formula (the A&S CND satisfies phi(-x) = 1 - phi(x) by construction,
+// SURVEY §8(c)-B), so it is the same value up to fp32 rounding.
+__device__ __forceinline__ void bs_price2(float2 S, float2 K, float2 T, float2 R, float2 V, float2 &call,
+                                          float2 &put) {
+    const float2 m1 = F2(-1.0f), one = F2(1.0f);
+    const float2 v2t = mul2(mul2(V, V), T);
+    const float2 rs = make_float2(rsqrtf(v2t.x), rsqrtf(v2t.y));                      // 1/(sigma sqrt T)
+    const float2 sst = mul2(v2t, rs);                                                  // sigma sqrt T
+    const float2 ert = mul2(mul2(R, T), F2(-1.44269504088896340736f));
+    const float2 kexp = mul2(K, make_float2(ex2_approx(ert.x), ex2_approx(ert.y)));  // K e^{-RT}
+    const float2 ratio = mul2(S, make_float2(__fdividef(1.0f, kexp.x), __fdividef(1.0f, kexp.y)));
+    const float2 lnr = mul2(make_float2(__log2f(ratio.x), __log2f(ratio.y)), F2(0.69314718055994530942f));
+    const float2 d1 = mul2(fma2(F2(0.5f), v2t, lnr), rs);
+    const float2 d2 = fma2(sst, m1, d1);
+    const float2 q1 = fma2(F2(0.2316419f), abs2(d1), one);
+    const float2 q2 = fma2(F2(0.2316419f), abs2(d2), one);
+    const float2 qq = mul2(q1, q2);
+    const float2 r = make_float2(__fdividef(1.0f, qq.x), __fdividef(1.0f, qq.y));     // both t = 1/q
+    const float2 ea = mul2(mul2(F2(-0.72134752044448170368f), d1), d1);
+    const float2 e1 = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));                 // e^{-d1^2/2}
+    const float2 e2 = mul2(e1, ratio);                                                 // e^{-d2^2/2}
+    const float2 w1 = mul2(e1, bs_poly2(mul2(q2, r)));
+    const float2 w2 = mul2(e2, bs_poly2(mul2(q1, r)));
+    const float2 om1 = fma2(w1, m1, one), om2 = fma2(w2, m1, one);
+    const float2 pd1 = make_float2(d1.x < 0.f ? w1.x : om1.x, d1.y < 0.f ? w1.y : om1.y);
+    const float2 pd2 = make_float2(d2.x < 0.f ? w2.x : om2.x, d2.y < 0.f ? w2.y : om2.y);
+    call = fma2(S, pd1, mul2(mul2(kexp, m1), pd2));
+    put = add2(call, fma2(S, m1, kexp));
+}
+
+__device__ __forceinline__ void bs_aparapi2(float2 u, float2 &call, float2 &put) {
+    const float2 S = fma2(F2(10.0f - 100.0f), u, F2(100.0f));
+    const float2 K = fma2(F2(10.0f - 100.0f), u, F2(100.0f));
+    const float2 T = fma2(F2(1.0f - 10.0f), u, F2(10.0f));
+    const float2 R = fma2(F2(0.01f - 0.05f), u, F2(0.05f));
+    const float2 V = fma2(F2(0.01f - 0.10f), u, F2(0.10f));
+    bs_price2(S, K, T, R, V, call, put);
+}
+
 // X = X_lo u + X_hi (1 - u) = X_hi + (X_lo - X_hi) u: one FFMA per parameter.
 __device__ __forceinline__ void bs_aparapi(float u, float &call, float &put) {
     const float S = fmaf(10.0f - 100.0f, u, 100.0f);
@@ -83,7 +145,8 @@ __device__ __forceinline__ void bs_aparapi(float u, float &call, float &put) {
     bs_price(S, K, T, R, V, call, put);
 }
 
-__global__ void __launch_bounds__(256) bs_v4_kernel(const float4 *__restrict__ u4, float4 *__restrict__ call4,
+template <int kDepth, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) bs_v4_kernel(const float4 *__restrict__ u4, float4 *__restrict__ call4,
                                                     float4 *__restrict__ put4, int64_t n4,
                                                     const float *__restrict__ ut, float *__restrict__ ct,
                                                     float *__restrict__ pt, int tail) {
@@ -91,7 +154,6 @@ __global__ void __launch_bounds__(256) bs_v4_kernel(const float4 *__restrict__ u
     // this trip's 4 * kDepth options are priced, so every thread always has
     // kDepth 128-bit loads in flight (the kernel is otherwise latency-bound:
     // ncu showed long-scoreboard stalls dominating with one load in flight).
-    constexpr int kDepth = 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     float4 nxt[kDepth];
@@ -110,13 +172,11 @@ __global__ void __launch_bounds__(256) bs_v4_kernel(const float4 *__restrict__ u
         for (int d = 0; d < kDepth; ++d) {
             const int64_t j = i + d * stride;
             if (j >= n4) break;
-            float4 c, p;
-            bs_aparapi(cur[d].x, c.x, p.x);
-            bs_aparapi(cur[d].y, c.y, p.y);
-            bs_aparapi(cur[d].z, c.z, p.z);
-            bs_aparapi(cur[d].w, c.w, p.w);
-            st_stream(call4 + j, c);
-            st_stream(put4 + j, p);
+            float2 c01, p01, c23, p23;
+            bs_aparapi2(make_float2(cur[d].x, cur[d].y), c01, p01);
+            bs_aparapi2(make_float2(cur[d].z, cur[d].w), c23, p23);
+            st_stream(call4 + j, make_float4(c01.x, c01.y, c23.x, c23.y));
+            st_stream(put4 + j, make_float4(p01.x, p01.y, p23.x, p23.y));
         }
     }
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -151,8 +211,10 @@ cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,
         // 8 consumer warps -- measured 163 us vs 155 us for this one: the
         // kernel is issue-bound once two loads per thread are in flight.)
         pick_grid(s, (n4 + 255) / 256, 8, 256, &grid, &block);
-        bs_v4_kernel<<<grid, block, 0, st>>>((const float4 *)u, (float4 *)call, (float4 *)put, n4, u + 4 * n4,
-                                             call + 4 * n4, put + 4 * n4, (int)(n - 4 * n4));
+        // 3 vectors in flight per thread, >= 3 blocks per SM (80 registers):
+        // measured 146 us vs 149 (2, 4 blocks), 149 (4, 2), 167 (2, 1)
+        bs_v4_kernel<3, 3><<<grid, block, 0, st>>>((const float4 *)u, (float4 *)call, (float4 *)put, n4,
+                                                   u + 4 * n4, call + 4 * n4, put + 4 * n4, (int)(n - 4 * n4));
     } else {
         pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
         bs_scalar_kernel<<<grid, block, 0, st>>>(u, call, put, n);
