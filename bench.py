@@ -403,6 +403,42 @@ def cfg1_latency(torch, J, reps=200):
         if mode.endswith("replay"):
             out[mode + "_graph_replays"] = int(st["graph_replays"])
         g.destroy()
+    # SURVEY §8(d) task-graph protocol: cold (first execute of a fresh graph:
+    # plan + device allocation + copies), warm (CACHABLE inputs resident, only
+    # the D2H of c and s), and the paper's K-iteration form (K
+    # iterations in one graph, one H2D per input and one D2H per output).
+    ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+    tc, ts = torch.empty(a.size, pin_memory=True), torch.empty(1, pin_memory=True)
+    g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=J.JACC_GRAPH_MERGE)
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R, True), g.a(tb, R, True), g.a(tc, W)])
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(tc, R), g.a(ts, W)])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g.run()
+    out["e2e_cold_us"] = (time.perf_counter() - t0) * 1e6
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        g.run()
+    out["e2e_warm_cachable_us"] = (time.perf_counter() - t0) / reps * 1e6
+    st = g.stats()
+    out["warm_copies"] = [int(st["h2d_count"]), int(st["d2h_count"])]
+    g.destroy()
+    K = 300
+    for mode, flags in {"kiter": 0, "kiter_merge_replay": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY}.items():
+        g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=flags)
+        for _ in range(K):
+            g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R), g.a(tb, R), g.a(tc, W)])
+            g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(tc, R), g.a(ts, W)])
+        for _ in range(3):
+            g.run()
+        t0 = time.perf_counter()
+        for _ in range(10):
+            g.run()
+        dt = (time.perf_counter() - t0) / 10
+        st = g.stats()
+        out[mode] = {"K": K, "graph_us": dt * 1e6, "us_per_iteration": dt / K * 1e6,
+                     "copies": [int(st["h2d_count"]), int(st["d2h_count"])]}
+        g.destroy()
     out["note"] = "host wall clock per jacc_graph_execute + jacc_graph_sync, mean of %d" % reps
     return out
 

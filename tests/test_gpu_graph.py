@@ -56,6 +56,42 @@ def test_cfg1_counted_copies_and_values():
     g.destroy()
 
 
+@pytest.mark.parametrize("flags", [0, "merge_replay"])
+def test_cfg1_k_iterations_one_graph(flags):
+    """Paper protocol (SURVEY §8(c)-G row 'cfg1 xK'): K iterations of
+    vadd -> reduce in ONE graph cost a single H2D per input and a single D2H
+    per output (naive: 3K / 2K), and the final values equal one iteration's."""
+    if flags == "merge_replay":
+        flags = J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY
+    n, K = 1 << 16, 40
+    a, b = synth.vadd_inputs(n, seed=5)
+    c = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
+    g = _graph(flags=flags)
+    for _ in range(K):
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+    for _ in range(2):   # second run exercises the replayed plan
+        c[:] = 0; s[:] = 0
+        g.run()
+        st = g.stats()
+        assert (st["h2d_count"], st["d2h_count"]) == (2, 2)
+        if not flags:
+            assert st["kernels"] == 2 * K
+        ref_c = oracle.vadd(a, b)
+        assert np.array_equal(c, ref_c)
+        ref, absum = oracle.reduce_sum(ref_c)
+        assert abs(s[0] - ref) <= 1e-4 * absum
+    g.destroy()
+    gn = _graph(flags=J.JACC_GRAPH_NAIVE)
+    for _ in range(K):
+        gn.add_task(J.JACC_OP_VADD_F32, [gn.a(a, R), gn.a(b, R), gn.a(c, W)])
+        gn.add_task(J.JACC_OP_REDUCE_SUM_F32, [gn.a(c, R), gn.a(s, W)])
+    gn.run()
+    st = gn.stats()
+    assert (st["h2d_count"], st["d2h_count"]) == (3 * K, 2 * K)
+    gn.destroy()
+
+
 def test_naive_equals_elided_and_counts():
     n = 100003
     a, b = synth.vadd_inputs(n, seed=3)
@@ -127,6 +163,41 @@ def test_serializability_random_dags():
                 assert np.all(np.abs(v - ref[k]) <= scale + 1e-6 * np.abs(ref[k])), (k, tasks)
         g.destroy()
         done += 1
+
+
+def test_state_machine_errors():
+    """the graph executes atomically -- no structural change or second
+    execute while EXECUTING; errors are status codes, never aborts."""
+    n = 4096
+    a, b = synth.vadd_inputs(n, seed=2)
+    c = np.zeros(n, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R, True), g.a(b, R), g.a(c, W)])
+    g.execute()
+    assert g.stats()["state"] == 1                       # EXECUTING
+    with pytest.raises(J.JaccError) as e:
+        g.execute()
+    assert e.value.status == J.JACC_ERR_STATE
+    with pytest.raises(J.JaccError) as e:
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+    assert e.value.status == J.JACC_ERR_STATE
+    with pytest.raises(J.JaccError) as e:
+        g.invalidate(a)
+    assert e.value.status == J.JACC_ERR_STATE
+    g.sync()
+    assert g.stats()["state"] == 2                       # DONE
+    assert np.array_equal(c, oracle.vadd(a, b))
+    with pytest.raises(J.JaccError) as e:
+        g.invalidate(np.zeros(3, np.float32))
+    assert e.value.status == J.JACC_ERR_NOT_FOUND
+    # DONE graphs are re-executable and can grow (state back to BUILDING)
+    s = np.zeros(1, np.float32)
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+    assert g.stats()["state"] == 0
+    g.run()
+    ref, absum = oracle.reduce_sum(c)
+    assert abs(s[0] - ref) <= 1e-4 * absum
+    g.destroy()
 
 
 def test_failure_leaves_host_untouched():
