@@ -370,6 +370,15 @@ def roofline_points(torch, J, peaks, reps=10):
     return out
 
 
+def _median_run_us(g, reps):
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        g.run()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts) * 1e6
+
+
 def cfg1_latency(torch, J, reps=200):
     """Task-graph time of BASELINE config 1 alone (vadd -> reduce, 2^20 f32):
     host wall clock per execute+sync, inputs device-resident, direct issue vs
@@ -395,10 +404,7 @@ def cfg1_latency(torch, J, reps=200):
         for _ in range(5):
             g.run()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            g.run()
-        out[mode + "_us"] = (time.perf_counter() - t0) / reps * 1e6
+        out[mode + "_us"] = _median_run_us(g, reps)
         st = g.stats()
         if mode.endswith("replay"):
             out[mode + "_graph_replays"] = int(st["graph_replays"])
@@ -416,10 +422,7 @@ def cfg1_latency(torch, J, reps=200):
     t0 = time.perf_counter()
     g.run()
     out["e2e_cold_us"] = (time.perf_counter() - t0) * 1e6
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        g.run()
-    out["e2e_warm_cachable_us"] = (time.perf_counter() - t0) / reps * 1e6
+    out["e2e_warm_cachable_us"] = _median_run_us(g, reps)
     st = g.stats()
     out["warm_copies"] = [int(st["h2d_count"]), int(st["d2h_count"])]
     g.destroy()
@@ -431,15 +434,12 @@ def cfg1_latency(torch, J, reps=200):
             g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(tc, R), g.a(ts, W)])
         for _ in range(3):
             g.run()
-        t0 = time.perf_counter()
-        for _ in range(10):
-            g.run()
-        dt = (time.perf_counter() - t0) / 10
+        dt = _median_run_us(g, 10) * 1e-6
         st = g.stats()
         out[mode] = {"K": K, "graph_us": dt * 1e6, "us_per_iteration": dt / K * 1e6,
                      "copies": [int(st["h2d_count"]), int(st["d2h_count"])]}
         g.destroy()
-    out["note"] = "host wall clock per jacc_graph_execute + jacc_graph_sync, mean of %d" % reps
+    out["note"] = "host wall clock per jacc_graph_execute + jacc_graph_sync, median of %d" % reps
     return out
 
 

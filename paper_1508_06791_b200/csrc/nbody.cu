@@ -6,11 +6,15 @@
 // tgt_offset .. tgt_offset + n_tgt - 1 (a rank's shard in SPMD, R17).
 //
 // sm_100a design (FP32-pipe bound: 12 fp32 ops + 1 MUFU.RSQ per interaction):
-//   * work unit = (64 threads x 6 targets) x (one chunk of kChunk = 8192
-//     sources); the chunk size depends on nothing but the source count, so
-//     every rank of a sharded run sums a target's sources in exactly the same
-//     groups as one GPU does (bitwise shard invariance, §8(e)), and 2^17
-//     bodies give ~5.5k units -- 37 per SM, the 148 SMs finish together;
+//   * work unit = (64 threads x 2P targets) x (one chunk of kChunk = 2048
+//     sources).  The chunk size is a constant, so every rank of a sharded run
+//     sums a target's sources in exactly the same groups as one GPU does
+//     (bitwise shard invariance, §8(e)); it is small so that even a 1/8
+//     shard has several waves of units (2^17 bodies: 21.9k units = 24.6 waves
+//     of 888 resident blocks; measured 6.54 ms vs 6.71 ms with 8192-source
+//     chunks = 6.2 waves).  Targets per thread (P pairs) only decide which
+//     thread computes a target, never the order of its sum, so P is chosen
+//     per launch from the wave count (P = 3 full size, P = 2 for shards);
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
 //     pairs of the paired FP32 instructions;
@@ -32,7 +36,7 @@ namespace {
 
 constexpr int kBlock = 64;
 constexpr int kTile = 256;                    // sources per shared-memory tile
-constexpr int kChunk = 8192;                  // sources per work unit
+constexpr int kChunk = 2048;                  // sources per work unit (fixed: shard invariance)
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
@@ -41,18 +45,51 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
+// Sum of one shared-memory tile of sources into the tile partials t* of the
+// thread's P target pairs, with the paired FP32 instructions (FADD2/FFMA2/
+// FMUL2, FMA-heavy pipe): per pair and source 3 FADD2 + 3 FFMA2 (r^2) +
+// 2 MUFU.RSQ + 3 FMUL2 (s = m inv^3) + 3 FFMA2 (t += d s).  kEqualMass: every
+// source of the tile has the same mass m, so m is factored out of the tile
+// sum -- s = inv^3 takes 2 FMUL2 (11 instead of 12 FP32 lane-ops per
+// interaction) and the caller scales the tile partial by m once.
+template <int P, int UNR, bool kEqualMass>
+__device__ __forceinline__ void tile_sum(const float4 *tile, const float2 (&nx)[P], const float2 (&ny)[P],
+                                         const float2 (&nz)[P], float2 e2, float2 (&tx)[P], float2 (&ty)[P],
+                                         float2 (&tz)[P]) {
+#pragma unroll UNR
+    for (int s = 0; s < kTile; ++s) {
+        const float4 A = tile[2 * s], B = tile[2 * s + 1];
+        const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float2 dx = __fadd2_rn(xj, nx[p]), dy = __fadd2_rn(yj, ny[p]), dz = __fadd2_rn(zj, nz[p]);
+            float2 r2 = __ffma2_rn(dx, dx, e2);
+            r2 = __ffma2_rn(dy, dy, r2);
+            r2 = __ffma2_rn(dz, dz, r2);
+            const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+            const float2 sc = kEqualMass ? __fmul2_rn(__fmul2_rn(inv, inv), inv)
+                                         : __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
+            tx[p] = __ffma2_rn(dx, sc, tx[p]);
+            ty[p] = __ffma2_rn(dy, sc, ty[p]);
+            tz[p] = __ffma2_rn(dz, sc, tz[p]);
+        }
+    }
+}
+
 // One work unit: kBlock * 2P targets x one chunk of sources.  Every thread
-// holds P target PAIRS and uses the paired FP32 instructions
-// (FADD2/FFMA2/FMUL2, FMA-heavy pipe) -- half the FP32 issue slots of scalar
-// code for the same arithmetic: per pair and source 12 paired ops + 2
-// MUFU.RSQ.  Target k of thread tid is t0 + tid + k * kBlock.
+// holds P target PAIRS (paired FP32 instructions: half the issue slots of
+// scalar code for the same arithmetic).  Target k of thread tid is
+// t0 + tid + k * kBlock.  Sources stream through shared memory one tile at a
+// time; a tile whose sources all have the same mass takes the equal-mass sum
+// (for a power-of-two mass, e.g. the workload's m = 1/N, its result is
+// bitwise identical to the general sum: scaling by 2^k commutes with every
+// rounding), any other tile (mixed masses, zero-mass padding) the general one.
 template <int P, int MINB, int UNR>
 __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
     constexpr int T = 2 * P;
-    constexpr int TW = 2;                 // float4 words per source in the tile
-    __shared__ float4 tile[TW * kTile];   // (x, x, y, y), (z, z, m, m)
+    __shared__ float4 tile[2 * kTile];    // per source: (x, x, y, y), (z, z, m, m)
     const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
     const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
     const int64_t j_end = min(j_begin + kChunk, n_src);
@@ -69,41 +106,39 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float
     }
     const float2 e2 = f2(eps2, eps2);
     for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
+        const float m0 = pos_src[j0].w;
+        bool same = true;
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < kTile / kBlock; ++q) {
             const int s = threadIdx.x + q * kBlock;
             const int64_t j = j0 + s;
             const float4 v = j < j_end ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-            tile[TW * s] = make_float4(v.x, v.x, v.y, v.y);
-            tile[TW * s + 1] = make_float4(v.z, v.z, v.w, v.w);
+            same &= v.w == m0;
+            tile[2 * s] = make_float4(v.x, v.x, v.y, v.y);
+            tile[2 * s + 1] = make_float4(v.z, v.z, v.w, v.w);
         }
-        __syncthreads();
+        const bool equal_mass = __syncthreads_and(same);
         float2 tx[P], ty[P], tz[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = f2(0.f, 0.f);
-#pragma unroll UNR
-        for (int s = 0; s < kTile; ++s) {
-            const float4 A = tile[TW * s], B = tile[TW * s + 1];
-            const float2 xj = f2(A.x, A.y), yj = f2(A.z, A.w), zj = f2(B.x, B.y), mj = f2(B.z, B.w);
+        if (equal_mass) {
+            tile_sum<P, UNR, true>(tile, nx, ny, nz, e2, tx, ty, tz);
+            const float2 m2 = f2(m0, m0);
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const float2 dx = __fadd2_rn(xj, nx[p]), dy = __fadd2_rn(yj, ny[p]), dz = __fadd2_rn(zj, nz[p]);
-                float2 r2 = __ffma2_rn(dx, dx, e2);
-                r2 = __ffma2_rn(dy, dy, r2);
-                r2 = __ffma2_rn(dz, dz, r2);
-                const float2 inv = f2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
-                const float2 sc = __fmul2_rn(__fmul2_rn(mj, inv), __fmul2_rn(inv, inv));
-                tx[p] = __ffma2_rn(dx, sc, tx[p]);
-                ty[p] = __ffma2_rn(dy, sc, ty[p]);
-                tz[p] = __ffma2_rn(dz, sc, tz[p]);
+                ax[p] = __ffma2_rn(tx[p], m2, ax[p]);
+                ay[p] = __ffma2_rn(ty[p], m2, ay[p]);
+                az[p] = __ffma2_rn(tz[p], m2, az[p]);
             }
-        }
+        } else {
+            tile_sum<P, UNR, false>(tile, nx, ny, nz, e2, tx, ty, tz);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            ax[p] = __fadd2_rn(ax[p], tx[p]);
-            ay[p] = __fadd2_rn(ay[p], ty[p]);
-            az[p] = __fadd2_rn(az[p], tz[p]);
+            for (int p = 0; p < P; ++p) {
+                ax[p] = __fadd2_rn(ax[p], tx[p]);
+                ay[p] = __fadd2_rn(ay[p], ty[p]);
+                az[p] = __fadd2_rn(az[p], tz[p]);
+            }
         }
     }
     float4 *out = part + (int64_t)blockIdx.y * n_tgt;
@@ -137,11 +172,34 @@ __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restr
 }
 
 typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
-struct Variant { partial_fn fn; int tpt; };
+struct Variant { partial_fn fn; int tpt; int occ; };
 
-// 3 target pairs per thread, source loop unrolled by 4: measured best on B200
-// at 2^17 bodies (ms/step: P=3 6.70, P=2 6.75, P=4 7.01; unroll 2/8 slower).
-Variant variant() { return Variant{nbody_partial_kernel<3, 1, 4>, 6}; }
+// Source loop unrolled by 4 (2 and 8 measured slower).  P = 3 pairs (148
+// registers, 6 blocks/SM) is the fastest per interaction at 2^17 bodies
+// (6.54 ms vs 6.67 for P = 2 at 10 blocks/SM, 7.0 for P = 4); P = 2 and
+// P = 1 give more, smaller units when a shard has few targets.  The variant
+// with the fewest waves x resident targets per SM wins (ties: larger P).
+Variant variant(int64_t n_tgt, int64_t nchunks) {
+    static Variant vs[3] = {{nbody_partial_kernel<3, 1, 4>, 6, 0}, {nbody_partial_kernel<2, 10, 4>, 4, 0},
+                            {nbody_partial_kernel<1, 16, 4>, 2, 0}};
+    static int sms = 0;
+    if (!sms) {
+        sms = sm_count();
+        for (Variant &v : vs)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v.occ, v.fn, kBlock, 0) != cudaSuccess || v.occ < 1)
+                v.occ = 1;
+    }
+    int best = 0;
+    double best_cost = 0;
+    for (int i = 0; i < 3; ++i) {
+        const int64_t per_block = (int64_t)kBlock * vs[i].tpt;
+        const int64_t units = (n_tgt + per_block - 1) / per_block * nchunks;
+        const int64_t slots = (int64_t)vs[i].occ * sms;
+        const double cost = (double)((units + slots - 1) / slots) * vs[i].occ * per_block;
+        if (i == 0 || cost < best_cost * 0.97) { best = i; best_cost = cost; }
+    }
+    return vs[best];
+}
 
 }  // namespace
 
@@ -160,7 +218,7 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
         cudaError_t e = cudaMemsetAsync(part, 0, n_tgt * sizeof(float4), st);
         if (e != cudaSuccess) return e;
     } else {
-        const Variant v = variant();
+        const Variant v = variant(n_tgt, nchunks);
         const int64_t per_block = (int64_t)kBlock * v.tpt;
         dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nchunks);
         v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--mode", default="3xtf32")
+    ap.add_argument("--shards", type=int, default=1, help="nbody: time rank 0's target shard of N/shards bodies")
     a = ap.parse_args()
     import torch
     import paper_1508_06791_b200 as J
@@ -72,10 +73,11 @@ def main():
         elif op == "nbody":
             n = a.n or synth.CFG5_N
             pos, vel = synth.nbody_state(n)
-            g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(D(pos), R, f32x4=True), g.a(D(vel), RW, f32x4=True),
-                                                   g.a(D(np.zeros_like(pos)), W, f32x4=True)],
-                       jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
-            units, kind = 20 * n * n, "TFLOP/s"
+            lo, hi = synth.shard_range(n, 0, a.shards)
+            g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(D(pos), R, f32x4=True), g.a(D(vel[lo:hi]), RW, f32x4=True),
+                                                   g.a(D(np.zeros_like(pos[lo:hi])), W, f32x4=True)],
+                       jacc.jacc_nbody_params_t(lo, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+            units, kind = 20 * n * (hi - lo), "TFLOP/s"
         elif op == "conv2d":
             n = a.n or 2048
             img = synth.uniform_f32(n * n, 11, -1, 1).reshape(n, n)

@@ -338,6 +338,42 @@ def test_nbody_steps(n, steps):
         assert (st["h2d_count"], st["d2h_count"]) == (2, 3)
 
 
+@pytest.mark.parametrize("case", ["mixed", "one_tile_mixed"])
+def test_nbody_unequal_masses(case):
+    """The kernel's general (per-source mass) tile path: masses that differ
+    across the whole set, or in one 256-source tile only (that tile takes
+    the general path, the others the equal-mass path)."""
+    n, steps = 5000, 3
+    pos, vel = synth.nbody_state(n, seed=77)
+    if case == "mixed":
+        pos[:, 3] = (synth.uniform_f32(n, 78, 0.5, 1.5) / n).astype(np.float32)
+    else:
+        pos[300, 3] = np.float32(3.0 / n)
+    gp, gv, _ = _nbody_graph(pos, vel, steps)
+    op, ov = oracle.nbody_steps(pos, vel, steps)
+    assert np.max(np.abs(gp[:, :3] - op[:, :3])) <= 1e-4
+    vs = np.mean(np.linalg.norm(ov[:, :3], axis=1))
+    assert np.max(np.abs(gv[:, :3] - ov[:, :3])) <= 1e-4 * vs
+
+
+def test_nbody_mass_scaling_exact():
+    """a is linear in the masses; doubling every mass (a power of two) must
+    double the step's velocity change bit for bit, on both tile paths."""
+    n = 3000
+    pos, vel = synth.nbody_state(n, seed=79)
+    outs = []
+    for scale in (1.0, 2.0):
+        for mixed in (False, True):
+            p = pos.copy()
+            p[:, 3] = np.float32(2.0 ** -12) * np.float32(scale)
+            if mixed:
+                p[::7, 3] *= np.float32(0.5)
+            _, gv, _ = _nbody_graph(p, vel, 1)
+            outs.append(gv[:, :3].copy())
+    assert np.array_equal(outs[2], 2 * outs[0])
+    assert np.array_equal(outs[3], 2 * outs[1])
+
+
 def test_nbody_full_size_one_step_sampled_and_momentum():
     n = synth.CFG5_N
     pos, vel = synth.nbody_state(n)
