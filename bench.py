@@ -212,6 +212,9 @@ class Suite:
                      [g.a(ALL, R, f32x4=True), g.a(V, RW, f32x4=True), g.a(L[(k + 1) % 2], W, f32x4=True)], prm)
         self.units["nbody"] = NBODY_FLOP * (hi - lo) * n5
         self.keep = keep
+        # named outputs (tests/test_gpu_bench_suite.py checks them against the oracle)
+        self.out = {"c": dc, "s": ds, "bins": dbins, "call": dcall, "put": dput, "C": dC,
+                    "pos": (P if world == 1 else L)[synth.CFG5_STEPS % 2], "vel": V}
 
     def all_streams(self):
         s = self.streams

@@ -162,12 +162,8 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
     if (!tc::make_map_2d(&ma, xa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tap, kp, kp, BM, BK, 128) ||
         !tc::make_map_2d(&mb, xb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tbp, kp, kp, BN, BK, 128))
         return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(corr_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = set_max_dyn_smem((const void *)corr_i8_kernel, kSmemBytes);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)(tbp / BN), (unsigned)(tap / BM));
     corr_i8_kernel<<<grid, kThreads, kSmemBytes, st>>>(ma, mb, C, ta, tb, (int)(kp / BK));
     ++*launches;

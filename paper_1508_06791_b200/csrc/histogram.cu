@@ -162,13 +162,8 @@ cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbi
     if (n <= 0) return cudaSuccess;
     int grid, block;
     if (nbins <= 256) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(hist256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 kSmemBytes);
-            if (e != cudaSuccess) return e;
-            attr_set = true;
-        }
+        cudaError_t e = set_max_dyn_smem((const void *)hist256_kernel, kSmemBytes);
+        if (e != cudaSuccess) return e;
         // unaligned head keys go to the edge path together with the tail
         int64_t head = (int64_t)(((16 - ((uintptr_t)keys & 15)) & 15) / 4);
         if (head > n) head = n;

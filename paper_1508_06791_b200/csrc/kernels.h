@@ -12,6 +12,11 @@
 namespace jacc_k {
 
 int sm_count();   // SMs of the current device (148 on B200), cached per device
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
+// thread-safe (graphs of different devices may launch from different threads)
+cudaError_t set_max_dyn_smem(const void *kernel, int bytes);
+// resident blocks per SM of `kernel` at `block` threads on the current device
+int blocks_per_sm(const void *kernel, int block, int dyn_smem);
 
 // c = a + b
 cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,

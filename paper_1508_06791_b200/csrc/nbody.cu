@@ -5,7 +5,7 @@
 // pos_src holds all n_src bodies (x, y, z, m); targets are bodies
 // tgt_offset .. tgt_offset + n_tgt - 1 (a rank's shard in SPMD, R17).
 //
-// sm_100a design (FP32-pipe bound: 12 fp32 ops + 1 MUFU.RSQ per interaction):
+// sm_100a design (FP32-pipe bound: 11-12 fp32 ops + 1 MUFU.RSQ per interaction):
 //   * work unit = (64 threads x 2P targets) x (one chunk of kChunk = 2048
 //     sources).  The chunk size is a constant, so every rank of a sharded run
 //     sums a target's sources in exactly the same groups as one GPU does
@@ -18,9 +18,10 @@
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
 //     pairs of the paired FP32 instructions;
-//   * each thread holds 3 target PAIRS in registers and uses the sm_100
-//     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops + 2 MUFU.RSQ per
-//     pair and source, half the FP32 issue slots of scalar code;
+//   * each thread holds P target PAIRS in registers and uses the sm_100
+//     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops (11 on equal-mass
+//     tiles) + 2 MUFU.RSQ per pair and source, half the FP32 issue slots of
+//     scalar code;
 //     measured alternatives (scalar FP32 on the other pipe for some targets,
 //     an lg2/ex2 path that moves work to the MUFU) were slower;
 //   * accumulation is TILE-PARTIAL (each tile summed separately, then added
@@ -180,23 +181,19 @@ struct Variant { partial_fn fn; int tpt; int occ; };
 // P = 1 give more, smaller units when a shard has few targets.  The variant
 // with the fewest waves x resident targets per SM wins (ties: larger P).
 Variant variant(int64_t n_tgt, int64_t nchunks) {
-    static Variant vs[3] = {{nbody_partial_kernel<3, 1, 4>, 6, 0}, {nbody_partial_kernel<2, 10, 4>, 4, 0},
-                            {nbody_partial_kernel<1, 16, 4>, 2, 0}};
-    static int sms = 0;
-    if (!sms) {
-        sms = sm_count();
-        for (Variant &v : vs)
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v.occ, v.fn, kBlock, 0) != cudaSuccess || v.occ < 1)
-                v.occ = 1;
-    }
+    Variant vs[3] = {{nbody_partial_kernel<3, 1, 4>, 6, 0}, {nbody_partial_kernel<2, 10, 4>, 4, 0},
+                     {nbody_partial_kernel<1, 16, 4>, 2, 0}};
+    const int sms = sm_count();
+    for (Variant &v : vs) v.occ = blocks_per_sm((const void *)v.fn, kBlock, 0);
     int best = 0;
     double best_cost = 0;
     for (int i = 0; i < 3; ++i) {
         const int64_t per_block = (int64_t)kBlock * vs[i].tpt;
+        if ((n_tgt + per_block - 1) / per_block > 0x7fffffff) continue;   // gridDim.x limit
         const int64_t units = (n_tgt + per_block - 1) / per_block * nchunks;
         const int64_t slots = (int64_t)vs[i].occ * sms;
         const double cost = (double)((units + slots - 1) / slots) * vs[i].occ * per_block;
-        if (i == 0 || cost < best_cost * 0.97) { best = i; best_cost = cost; }
+        if (best_cost == 0 || cost < best_cost * 0.97) { best = i; best_cost = cost; }
     }
     return vs[best];
 }
@@ -220,6 +217,7 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
     } else {
         const Variant v = variant(n_tgt, nchunks);
         const int64_t per_block = (int64_t)kBlock * v.tpt;
+        if (nchunks > 65535) return cudaErrorInvalidConfiguration;   // > 134M sources: shard further
         dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nchunks);
         v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);
         ++*launches;

@@ -188,8 +188,8 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
         return JACC_OK;
     };
     auto acc = [&](int i, uint32_t allowed_mask) -> int {
-        // allowed_mask: bit (1 << access)
-        if (!((1u << a[i].access) & allowed_mask))
+        // allowed_mask: bit (1 << access); access is READ, WRITE or READWRITE
+        if (a[i].access < JACC_READ || a[i].access > JACC_READWRITE || !((1u << a[i].access) & allowed_mask))
             return fail(JACC_ERR_ACCESS, "%s arg %d: access %u not allowed", op_name(op), i, a[i].access);
         return JACC_OK;
     };
@@ -287,7 +287,7 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             const jacc_conv2d_params_t *p = (const jacc_conv2d_params_t *)params;
             if (p->radius < 1 || p->radius > 4) return fail(JACC_ERR_UNSUPPORTED, "conv2d: radius %d", p->radius);
             const uint64_t k = 2 * p->radius + 1;
-            if (p->H < 0 || p->W < 0 || a[0].count != (uint64_t)(p->H * p->W) || a[2].count != a[0].count ||
+            if (p->H < 0 || p->W < 0 || a[0].count != (uint64_t)p->H * (uint64_t)p->W || a[2].count != a[0].count ||
                 a[1].count != k * k)
                 return fail(JACC_ERR_INVALID_ARG, "conv2d: counts do not match H x W / filter size");
             break;
@@ -297,8 +297,8 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             for (int i = 0; i < 3; ++i) T(dt(i, JACC_I32));
             if (!params || psz < sizeof(jacc_corr_params_t)) return fail(JACC_ERR_INVALID_ARG, "corr: params");
             const jacc_corr_params_t *p = (const jacc_corr_params_t *)params;
-            if (p->ta < 0 || p->tb < 0 || p->words < 0 || a[0].count != (uint64_t)(p->ta * p->words) ||
-                a[1].count != (uint64_t)(p->tb * p->words) || a[2].count != (uint64_t)(p->ta * p->tb))
+            if (p->ta < 0 || p->tb < 0 || p->words < 0 || a[0].count != (uint64_t)p->ta * (uint64_t)p->words ||
+                a[1].count != (uint64_t)p->tb * (uint64_t)p->words || a[2].count != (uint64_t)p->ta * (uint64_t)p->tb)
                 return fail(JACC_ERR_INVALID_ARG, "corr: counts do not match ta, tb, words");
             break;
         }

@@ -327,13 +327,8 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
     if (!make_map(&m_ahi, ahi, Mp, Kp, BM) || !make_map(&m_alo, alo, Mp, Kp, BM) ||
         !make_map(&m_bhi, bhi, Np, Kp, BN) || !make_map(&m_blo, blo, Np, Kp, BN))
         return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = set_max_dyn_smem((const void *)gemm_3xtf32_kernel, kSmemBytes);
+    if (e != cudaSuccess) return e;
     const int num_m = (int)(Mp / BM), num_n = (int)(Np / BN);
     gemm_3xtf32_kernel<<<num_m * num_n, kThreads, kSmemBytes, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc,
                                                            (int)(Kp / BK), num_m, num_n);

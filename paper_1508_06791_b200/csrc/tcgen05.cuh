@@ -88,14 +88,14 @@ typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 inline encode_fn_t get_encode() {
-    static encode_fn_t fn = nullptr;
-    if (!fn) {
+    static const encode_fn_t fn = [] {   // thread-safe one-time init
         void *p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = (encode_fn_t)p;
-    }
+            return (encode_fn_t)p;
+        return (encode_fn_t) nullptr;
+    }();
     return fn;
 }
 

@@ -81,6 +81,17 @@ def test_add_task_validation():
         arr = (jacc.jacc_arg_t * 3)(g.a(a, 1), g.a(b, 1), g.a(c, 2))
         J.check(J.jacc_graph_add_task(g._h, J.JACC_OP_VADD_F32, arr, 3, None, 0, None, 3, None), "x")
     assert e.value.status == J.JACC_ERR_DEVICE
+    for bad in (0, 4, 33, 0xFFFFFFFF):      # access outside READ/WRITE/READWRITE
+        with pytest.raises(J.JaccError) as e:
+            arr = (jacc.jacc_arg_t * 3)(g.a(a, 1), g.a(b, 1), g.a(c, 2))
+            arr[2].access = bad
+            J.check(J.jacc_graph_add_task(g._h, J.JACC_OP_VADD_F32, arr, 3, None, 0, None, 0, None), "x")
+        assert e.value.status == J.JACC_ERR_ACCESS
+    img = np.zeros((4, 4), np.float32); f = np.zeros(25, np.float32)
+    with pytest.raises(J.JaccError) as e:   # H*W that overflows int32 must not wrap around
+        g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, 1), g.a(f, 1), g.a(np.zeros_like(img), 2)],
+                   jacc.jacc_conv2d_params_t(65536, 65536, 2, 0))
+    assert e.value.status == J.JACC_ERR_INVALID_ARG
     keys = np.zeros(64, np.int32); bins = np.zeros(300, np.int32)
     with pytest.raises(J.JaccError):        # bins count != nbins
         g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, 1), g.a(bins, 2)], jacc.jacc_hist_params_t(256))

@@ -1,0 +1,92 @@
+"""Parity of the graph bench.py times, in the launch configuration it times
+(task ③ "at BASELINE.json's full sizes, in the launch
+configuration bench.py times"): the jacc-suite graph at full size, both the
+device-resident form (JACC_GRAPH_SERIAL, the timed region) and the pinned
+host-buffer form (4 compute streams, the e2e region), checked against the
+oracle on sampled outputs and, where the oracle cannot follow at this size
+(10 N-body steps of 2^17 bodies), against invariants; and the two forms must
+agree bit for bit (schedule invariance of every kernel).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+J = pytest.importorskip("paper_1508_06791_b200")
+from paper_1508_06791_b200 import jacc  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def _np(t):
+    return t.cpu().numpy() if t.is_cuda else t.numpy()
+
+
+@pytest.fixture(scope="module")
+def suite_outputs():
+    outs = {}
+    for form, host, flags in (("device", False, J.JACC_GRAPH_SERIAL), ("host", True, 0)):
+        s = bench.Suite(torch, J, jacc, 0, 1, 0, host_mode=host, sgemm_mode=J.JACC_SGEMM_3XTF32, flags=flags)
+        s.g.run()
+        st = s.g.stats()
+        outs[form] = ({k: _np(v).copy() for k, v in s.out.items()}, st)
+        s.g.destroy()
+        del s
+        torch.cuda.empty_cache()
+    return outs
+
+
+def test_suite_forms_bitwise_equal(suite_outputs):
+    dev, _ = suite_outputs["device"]
+    host, st = suite_outputs["host"]
+    for k in dev:
+        assert np.array_equal(dev[k], host[k]), k
+    # host form: every input copied in once, every output out once (SURVEY count table)
+    assert st["h2d_count"] == 8 and st["d2h_count"] == 9
+
+
+def test_suite_cfg1_cfg2(suite_outputs):
+    o, _ = suite_outputs["device"]
+    a, b = synth.vadd_inputs()
+    c = oracle.vadd(a, b)
+    assert np.array_equal(o["c"], c)
+    ref, absum = oracle.reduce_sum(c)
+    assert abs(float(o["s"][0]) - ref) <= 1e-4 * absum
+    keys = synth.hist_keys()
+    assert np.array_equal(o["bins"], oracle.histogram(keys, 256))
+
+
+def test_suite_cfg3_cfg4_sampled(suite_outputs):
+    o, _ = suite_outputs["device"]
+    u = synth.bs_rand()
+    idx = np.concatenate([synth.rng(31).integers(0, u.size, 1 << 15), [0, u.size - 1]])
+    oc, op = oracle.blackscholes(u[idx])
+    uu = u[idx].astype(np.float64)
+    S = 10 * uu + 100 * (1 - uu); T = uu + 10 * (1 - uu); Rr = 0.01 * uu + 0.05 * (1 - uu)
+    scale = S + S * np.exp(-Rr * T)          # S + K e^{-RT}, K = S (R12)
+    assert np.max(np.abs(o["call"][idx] - oc) / scale) <= 1e-5
+    assert np.max(np.abs(o["put"][idx] - op) / scale) <= 1e-5
+    n = synth.CFG4_MNK
+    A, B = synth.sgemm_inputs(n, n, n)
+    rows = np.concatenate([synth.rng(32).integers(0, n, 6), [0, n - 1]])
+    R = oracle.sgemm_rows(A, B, rows)
+    assert np.max(np.abs(o["C"][rows] - R) / np.abs(R)) <= 1e-4
+
+
+def test_suite_cfg5_invariants(suite_outputs):
+    """10 steps of 2^17 bodies: momentum conserved (Σ m v = 0 from rest),
+    masses carried unchanged, every body moved by at most |v|max·10·dt."""
+    o, _ = suite_outputs["device"]
+    pos0, _ = synth.nbody_state()
+    pos, vel = o["pos"].astype(np.float64), o["vel"].astype(np.float64)
+    m = pos0[:, 3:4].astype(np.float64)
+    p_tot = np.sum(m * vel[:, :3], axis=0)
+    assert np.max(np.abs(p_tot)) <= 1e-5 * np.sum(m * np.abs(vel[:, :3]))
+    assert np.array_equal(o["pos"][:, 3], pos0[:, 3])
+    vmax = np.max(np.linalg.norm(vel[:, :3], axis=1))
+    disp = np.linalg.norm(pos[:, :3] - pos0[:, :3].astype(np.float64), axis=1)
+    assert np.all(np.isfinite(pos)) and np.max(disp) <= vmax * synth.CFG5_STEPS * synth.NBODY_DT * 1.0001
