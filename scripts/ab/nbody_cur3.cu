@@ -17,9 +17,9 @@
 //     per launch from the wave count (P = 3 full size, P = 2 for shards);
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
-//     pairs of the paired FP32 instructions; grids only a few waves deep
-//     (target shards) use a double-buffered kernel, the next tile arriving
-//     by cp.async while the current one is summed;
+//     pairs of the paired FP32 instructions; double-buffered, the next
+//     tile arriving by cp.async while the current one is summed (one
+//     barrier per tile, no exposed L2 latency);
 //   * each thread holds P target PAIRS in registers and uses the sm_100
 //     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops (11 on equal-mass
 //     tiles) + 2 MUFU.RSQ per pair and source, half the FP32 issue slots of
@@ -289,35 +289,34 @@ struct Variant { partial_fn fn; int tpt; };
 // (6.54 ms vs 6.67 for P = 2 at 10 blocks/SM, 7.0 for P = 4); P = 2 and
 // P = 1 give more, smaller units when a shard has few targets.  The variant
 // with the fewest waves x resident targets per SM wins (ties: larger P);
-// grids under 16 waves (of the P = 3 single-buffered kernel) choose among
-// the double-buffered kernels.
+// grids under 16 waves take the double-buffered kernel when it does not
+// lower the occupancy.
 Variant variant(int64_t n_tgt, int64_t nchunks) {
-    const Variant single[3] = {{nbody_partial_kernel<3, 1, 4>, 6}, {nbody_partial_kernel<2, 10, 4>, 4},
+    const Variant single[3] = {{nbody_partial_kernel<3, 1, 4>, 6},
+                               {nbody_partial_kernel<2, 10, 4>, 4},
                                {nbody_partial_kernel<1, 16, 4>, 2}};
-    const Variant dbl[3] = {{nbody_partial_db_kernel<3, 1, 4>, 6}, {nbody_partial_db_kernel<2, 10, 4>, 4},
+    const Variant dbl[3] = {{nbody_partial_db_kernel<3, 1, 4>, 6},
+                            {nbody_partial_db_kernel<2, 10, 4>, 4},
                             {nbody_partial_db_kernel<1, 16, 4>, 2}};
     const int sms = sm_count();
-    // waves of a family's variant i, and its cost = waves (rounded up) x
-    // resident targets per SM (the time of one wave is ~ proportional to it)
-    auto waves = [&](const Variant *fam, int i, double *cost) -> double {
-        const int occ = blocks_per_sm((const void *)fam[i].fn, kBlock, 0);
-        const int64_t per_block = (int64_t)kBlock * fam[i].tpt;
+    int best = -1;
+    double best_cost = 0, best_waves = 0;
+    for (int i = 0; i < 3; ++i) {
+        const int occ = blocks_per_sm((const void *)single[i].fn, kBlock, 0);
+        const int64_t per_block = (int64_t)kBlock * single[i].tpt;
+        if ((n_tgt + per_block - 1) / per_block > 0x7fffffff) continue;   // gridDim.x limit
         const int64_t units = (n_tgt + per_block - 1) / per_block * nchunks;
         const int64_t slots = (int64_t)occ * sms;
-        *cost = (double)((units + slots - 1) / slots) * occ * per_block;
-        return (double)units / slots;
-    };
-    double c;
-    const bool deep = waves(single, 0, &c) >= 16.0;   // many waves: every SM stays full
-    const Variant *fam = deep ? single : dbl;
-    int best = 0;
-    double best_cost = 0;
-    for (int i = 0; i < 3; ++i) {
-        if ((n_tgt + (int64_t)kBlock * fam[i].tpt - 1) / ((int64_t)kBlock * fam[i].tpt) > 0x7fffffff) continue;
-        waves(fam, i, &c);
-        if (best_cost == 0 || c < best_cost * 0.97) { best = i; best_cost = c; }
+        const double cost = (double)((units + slots - 1) / slots) * occ * per_block;
+        if (best < 0 || cost < best_cost * 0.97) { best = i; best_cost = cost; best_waves = (double)units / slots; }
     }
-    return fam[best];
+    if (best < 0) best = 0;
+    // double buffering only where it keeps the occupancy (its 21 KB of shared
+    // memory would cut P = 1 from 16 to 10 blocks/SM)
+    if (best_waves < 16.0 && blocks_per_sm((const void *)dbl[best].fn, kBlock, 0) >=
+                                 blocks_per_sm((const void *)single[best].fn, kBlock, 0))
+        return dbl[best];
+    return single[best];
 }
 
 }  // namespace

@@ -17,9 +17,9 @@
 //     per launch from the wave count (P = 3 full size, P = 2 for shards);
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
-//     pairs of the paired FP32 instructions; grids only a few waves deep
-//     (target shards) use a double-buffered kernel, the next tile arriving
-//     by cp.async while the current one is summed;
+//     pairs of the paired FP32 instructions; double-buffered, the next
+//     tile arriving by cp.async while the current one is summed (one
+//     barrier per tile, no exposed L2 latency);
 //   * each thread holds P target PAIRS in registers and uses the sm_100
 //     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops (11 on equal-mass
 //     tiles) + 2 MUFU.RSQ per pair and source, half the FP32 issue slots of

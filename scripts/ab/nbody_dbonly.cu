@@ -17,9 +17,9 @@
 //     per launch from the wave count (P = 3 full size, P = 2 for shards);
 //   * sources stream through shared memory in tiles of 256, stored
 //     duplicated as (x,x,y,y),(z,z,m,m) so one LDS.128 yields the operand
-//     pairs of the paired FP32 instructions; grids only a few waves deep
-//     (target shards) use a double-buffered kernel, the next tile arriving
-//     by cp.async while the current one is summed;
+//     pairs of the paired FP32 instructions; double-buffered, the next
+//     tile arriving by cp.async while the current one is summed (one
+//     barrier per tile, no exposed L2 latency);
 //   * each thread holds P target PAIRS in registers and uses the sm_100
 //     FADD2/FFMA2/FMUL2 (FMA-heavy pipe): 12 paired ops (11 on equal-mass
 //     tiles) + 2 MUFU.RSQ per pair and source, half the FP32 issue slots of
@@ -89,81 +89,6 @@ __device__ __forceinline__ void tile_sum(const float4 *tile, const float2 (&nx)[
 // rounding), any other tile (mixed masses, zero-mass padding) the general one.
 template <int P, int MINB, int UNR>
 __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
-                                                               int64_t n_tgt, int64_t tgt_offset, float eps2,
-                                                               float4 *__restrict__ part) {
-    constexpr int T = 2 * P;
-    __shared__ float4 tile[2 * kTile];    // per source: (x, x, y, y), (z, z, m, m)
-    const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
-    const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
-    const int64_t j_end = min(j_begin + kChunk, n_src);
-    float2 nx[P], ny[P], nz[P], ax[P], ay[P], az[P];    // nx = -x of the target pair
-    auto load_t = [&](int k) {
-        const int64_t t = t0 + threadIdx.x + k * kBlock;
-        return t < n_tgt ? pos_src[tgt_offset + t] : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const float4 a = load_t(2 * p), b = load_t(2 * p + 1);
-        nx[p] = f2(-a.x, -b.x); ny[p] = f2(-a.y, -b.y); nz[p] = f2(-a.z, -b.z);
-        ax[p] = ay[p] = az[p] = f2(0.f, 0.f);
-    }
-    const float2 e2 = f2(eps2, eps2);
-    for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
-        const float m0 = pos_src[j0].w;
-        bool same = true;
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kTile / kBlock; ++q) {
-            const int s = threadIdx.x + q * kBlock;
-            const int64_t j = j0 + s;
-            const float4 v = j < j_end ? pos_src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-            same &= v.w == m0;
-            tile[2 * s] = make_float4(v.x, v.x, v.y, v.y);
-            tile[2 * s + 1] = make_float4(v.z, v.z, v.w, v.w);
-        }
-        const bool equal_mass = __syncthreads_and(same);
-        float2 tx[P], ty[P], tz[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = f2(0.f, 0.f);
-        if (equal_mass) {
-            tile_sum<P, UNR, true>(tile, nx, ny, nz, e2, tx, ty, tz);
-            const float2 m2 = f2(m0, m0);
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                ax[p] = __ffma2_rn(tx[p], m2, ax[p]);
-                ay[p] = __ffma2_rn(ty[p], m2, ay[p]);
-                az[p] = __ffma2_rn(tz[p], m2, az[p]);
-            }
-        } else {
-            tile_sum<P, UNR, false>(tile, nx, ny, nz, e2, tx, ty, tz);
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                ax[p] = __fadd2_rn(ax[p], tx[p]);
-                ay[p] = __fadd2_rn(ay[p], ty[p]);
-                az[p] = __fadd2_rn(az[p], tz[p]);
-            }
-        }
-    }
-    float4 *out = part + (int64_t)blockIdx.y * n_tgt;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const int64_t ta = t0 + threadIdx.x + (2 * p) * kBlock, tb = ta + kBlock;
-        if (ta < n_tgt) out[ta] = make_float4(ax[p].x, ay[p].x, az[p].x, 0.f);
-        if (tb < n_tgt) out[tb] = make_float4(ax[p].y, ay[p].y, az[p].y, 0.f);
-    }
-}
-
-// Double-buffered variant of the kernel above: two tile buffers, the next
-// tile's raw float4s arriving by cp.async into `stage` while the current tile
-// is summed, one barrier per tile.  Measured (ms per step at 2^17 bodies,
-// target shards 1/2/4/8): single 6.103 / 3.382 / 1.724 / 0.836, double
-// 6.201 / 3.104 / 1.651 / 0.846 -- double buffering pays when the grid is
-// only a few waves deep (SMs then hold few blocks and a tile load's L2
-// latency is not covered by the others); its per-tile overhead costs 1.5 %
-// when many waves keep every SM full.  (Kept as a separate kernel: a merged
-// template with both loops compiled 2 % slower in both modes.)
-template <int P, int MINB, int UNR>
-__global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
                                                                int64_t n_tgt, int64_t tgt_offset, float eps2,
                                                                float4 *__restrict__ part) {
     constexpr int T = 2 * P;
@@ -282,42 +207,29 @@ __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restr
 }
 
 typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
-struct Variant { partial_fn fn; int tpt; };
+struct Variant { partial_fn fn; int tpt; int occ; };
 
-// Source loop unrolled by 4 (2 and 8 measured slower).  P = 3 pairs (152
+// Source loop unrolled by 4 (2 and 8 measured slower).  P = 3 pairs (148
 // registers, 6 blocks/SM) is the fastest per interaction at 2^17 bodies
 // (6.54 ms vs 6.67 for P = 2 at 10 blocks/SM, 7.0 for P = 4); P = 2 and
 // P = 1 give more, smaller units when a shard has few targets.  The variant
-// with the fewest waves x resident targets per SM wins (ties: larger P);
-// grids under 16 waves (of the P = 3 single-buffered kernel) choose among
-// the double-buffered kernels.
+// with the fewest waves x resident targets per SM wins (ties: larger P).
 Variant variant(int64_t n_tgt, int64_t nchunks) {
-    const Variant single[3] = {{nbody_partial_kernel<3, 1, 4>, 6}, {nbody_partial_kernel<2, 10, 4>, 4},
-                               {nbody_partial_kernel<1, 16, 4>, 2}};
-    const Variant dbl[3] = {{nbody_partial_db_kernel<3, 1, 4>, 6}, {nbody_partial_db_kernel<2, 10, 4>, 4},
-                            {nbody_partial_db_kernel<1, 16, 4>, 2}};
+    Variant vs[3] = {{nbody_partial_kernel<3, 1, 4>, 6, 0}, {nbody_partial_kernel<2, 10, 4>, 4, 0},
+                     {nbody_partial_kernel<1, 16, 4>, 2, 0}};
     const int sms = sm_count();
-    // waves of a family's variant i, and its cost = waves (rounded up) x
-    // resident targets per SM (the time of one wave is ~ proportional to it)
-    auto waves = [&](const Variant *fam, int i, double *cost) -> double {
-        const int occ = blocks_per_sm((const void *)fam[i].fn, kBlock, 0);
-        const int64_t per_block = (int64_t)kBlock * fam[i].tpt;
-        const int64_t units = (n_tgt + per_block - 1) / per_block * nchunks;
-        const int64_t slots = (int64_t)occ * sms;
-        *cost = (double)((units + slots - 1) / slots) * occ * per_block;
-        return (double)units / slots;
-    };
-    double c;
-    const bool deep = waves(single, 0, &c) >= 16.0;   // many waves: every SM stays full
-    const Variant *fam = deep ? single : dbl;
+    for (Variant &v : vs) v.occ = blocks_per_sm((const void *)v.fn, kBlock, 0);
     int best = 0;
     double best_cost = 0;
     for (int i = 0; i < 3; ++i) {
-        if ((n_tgt + (int64_t)kBlock * fam[i].tpt - 1) / ((int64_t)kBlock * fam[i].tpt) > 0x7fffffff) continue;
-        waves(fam, i, &c);
-        if (best_cost == 0 || c < best_cost * 0.97) { best = i; best_cost = c; }
+        const int64_t per_block = (int64_t)kBlock * vs[i].tpt;
+        if ((n_tgt + per_block - 1) / per_block > 0x7fffffff) continue;   // gridDim.x limit
+        const int64_t units = (n_tgt + per_block - 1) / per_block * nchunks;
+        const int64_t slots = (int64_t)vs[i].occ * sms;
+        const double cost = (double)((units + slots - 1) / slots) * vs[i].occ * per_block;
+        if (best_cost == 0 || cost < best_cost * 0.97) { best = i; best_cost = cost; }
     }
-    return fam[best];
+    return vs[best];
 }
 
 }  // namespace

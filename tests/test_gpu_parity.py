@@ -356,6 +356,36 @@ def test_nbody_unequal_masses(case):
     assert np.max(np.abs(gv[:, :3] - ov[:, :3])) <= 1e-4 * vs
 
 
+def test_nbody_full_size_mixed_masses_and_kernel_variants():
+    """2^17 bodies: the full grid takes the single-buffered kernel (many
+    waves), a 1/2 and a 1/8 target shard the double-buffered one (few waves,
+    P = 3 and P = 2) -- with unequal masses (general tile path) the sampled
+    accelerations match the oracle, and every shard is bitwise equal to the
+    full run's slice (the same chunk and tile grouping in every variant)."""
+    n = synth.CFG5_N
+    pos, vel = synth.nbody_state(n, seed=81)
+    pos[:, 3] = (synth.uniform_f32(n, 82, 0.5, 1.5) / n).astype(np.float32)
+    prm = lambda lo: jacc.jacc_nbody_params_t(lo, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G)
+    dpos = _dev(pos)
+
+    def step(lo, hi):
+        dv = _dev(vel[lo:hi]); out = torch.zeros_like(dv)
+        g = _graph()
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(dpos, R, f32x4=True), g.a(dv, RW, f32x4=True),
+                                               g.a(out, W, f32x4=True)], prm(lo))
+        g.run(); g.destroy()
+        return dv.cpu().numpy(), out.cpu().numpy()
+    full_v, full_p = step(0, n)
+    idx = np.concatenate([synth.rng(83).integers(0, n, 48), [0, n - 1]])
+    a_ref = oracle.nbody_accel(pos.astype(np.float64), idx)
+    a_gpu = full_v[idx, :3].astype(np.float64) / synth.NBODY_DT
+    assert np.max(np.linalg.norm(a_gpu - a_ref, axis=1) / np.linalg.norm(a_ref, axis=1)) <= 1e-4
+    for k, r in ((2, 1), (8, 5)):
+        lo, hi = synth.shard_range(n, r, k)
+        v, p = step(lo, hi)
+        assert np.array_equal(v, full_v[lo:hi]) and np.array_equal(p, full_p[lo:hi]), (k, r)
+
+
 def test_nbody_mass_scaling_exact():
     """a is linear in the masses; doubling every mass (a power of two) must
     double the step's velocity change bit for bit, on both tile paths."""
