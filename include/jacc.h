@@ -136,7 +136,9 @@ typedef enum jacc_op {
      * args: pos_src:R f32x4[n_src] (x, y, z, m of ALL bodies),
      *       vel:RW f32x4[n_tgt] (vx, vy, vz, 0 of the targets),
      *       pos_out:W f32x4[n_tgt] (x, y, z, m of the targets after the step);
-     * target i is body tgt_offset + i of pos_src.  params jacc_nbody_params_t. */
+     * target i is body tgt_offset + i of pos_src.  params jacc_nbody_params_t
+     * (eps2 > 0).  n_src <= 65535 * 2048 per task (JACC_ERR_UNSUPPORTED
+     * beyond: shard the sources' chunks over tasks/ranks).                 */
     JACC_OP_NBODY_STEP_F32 = 7,
     /* Collectives over the graph's NCCL communicator (north_star; SPMD, one
      * process per GPU, reading R17).  world == 1 without a communicator is

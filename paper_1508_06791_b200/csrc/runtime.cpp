@@ -260,6 +260,9 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             if (p->tgt_offset < 0 || (uint64_t)p->tgt_offset + a[1].count > a[0].count)
                 return fail(JACC_ERR_INVALID_ARG, "nbody: targets outside pos_src");
             if (!(p->eps2 > 0.f)) return fail(JACC_ERR_INVALID_ARG, "nbody: eps2 must be > 0");
+            if (a[0].count > (uint64_t)65535 * 2048)
+                return fail(JACC_ERR_UNSUPPORTED, "nbody: %llu sources > 65535 chunks of 2048",
+                            (unsigned long long)a[0].count);
             break;
         }
         case JACC_OP_ALLREDUCE_SUM:

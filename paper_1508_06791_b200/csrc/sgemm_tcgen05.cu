@@ -15,12 +15,13 @@
 //   2. split_bt: B (K x N, ldb) -> B_hi^T, B_lo^T [Np x Kp] (transposed through
 //      shared memory so both UMMA operands are K-major), zero padded;
 //   3. gemm: one 128 x 256 output tile per CTA, warp-specialised --
-//        warp 0     TMA producer: per 32-wide K block, 4 boxes (A_hi, A_lo:
-//                   128x32; B_hi, B_lo: 256x32) into a 2-stage mbarrier ring,
-//                   128B-swizzled;
+//        warp 0     TMA producer: per 16-wide K block, 4 boxes (A_hi, A_lo:
+//                   128x16; B_hi, B_lo: 256x16) into a 4-stage mbarrier ring
+//                   (48 KB per stage), 64B-swizzled;
 //        warp 1     TMEM allocator + single-thread MMA issuer: per K block
-//                   4 k-steps x 3 tcgen05.mma.cta_group::1.kind::tf32
-//                   (M=128, N=256, K=8), D in TMEM (256 fp32 columns);
+//                   2 k-steps x 3 tcgen05.mma.cta_group::1.kind::tf32
+//                   (M=128, N=256, K=8), D in TMEM: two 256-column fp32
+//                   accumulators used alternately per 256-wide K chunk;
 //                   tcgen05.commit frees the smem stage / signals the epilogue;
 //        warps 2..9 epilogue: every 256 K, tcgen05.ld 32x32b.x32 TMEM ->
 //                   registers, fp32 round-to-nearest accumulation of the
