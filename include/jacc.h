@@ -127,7 +127,9 @@ typedef enum jacc_op {
     JACC_OP_BLACKSCHOLES_SOA_F32 = 5,
     /* C = A.B, row-major, beta = 0 (reading R13).
      * args: A:R f32[M*lda], B:R f32[K*ldb], C:W f32[M*ldc];
-     * params jacc_sgemm_params_t.                                           */
+     * params jacc_sgemm_params_t.  Only the M x N window of C is written; as
+     * for every W argument (never uploaded), the rest of the buffer is
+     * undefined after execute.                                              */
     JACC_OP_SGEMM_F32 = 6,
     /* One symplectic-Euler step of softened direct-sum gravity (north_star;
      * not in the paper, reading R16):

@@ -305,13 +305,8 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
                          cudaStream_t st, int *launches) {
     const int64_t M = p->M, N = p->N, K = p->K;
     if (M == 0 || N == 0) return cudaSuccess;
-    if (K == 0) {   // C = 0
-        for (int64_t r = 0; r < M; ++r) {
-            cudaError_t e = cudaMemsetAsync(C + r * p->ldc, 0, N * 4, st);
-            if (e != cudaSuccess) return e;
-        }
-        return cudaSuccess;
-    }
+    if (K == 0)   // C = 0 (beta = 0): the M x N window only
+        return cudaMemset2DAsync(C, (size_t)p->ldc * 4, 0, (size_t)N * 4, (size_t)M, st);
     const int64_t Mp = round_up(M, BM), Np = round_up(N, BN), Kp = round_up(K, BK);
     float *ahi = (float *)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
     float *alo = ahi + Mp * Kp;

@@ -268,6 +268,32 @@ SG_SHAPES = [(1, 1, 1), (127, 129, 65), (256, 256, 256), (300, 520, 1000), (1024
 
 
 @pytest.mark.parametrize("mode", [J.JACC_SGEMM_FFMA, J.JACC_SGEMM_3XTF32], ids=["ffma", "3xtf32"])
+def test_sgemm_strided_and_degenerate(mode):
+    """Leading dimensions larger than the logical widths (sub-matrix views of
+    padded storage, P:525 row-major with lda/ldb/ldc), and K = 0 (C = 0,
+    beta = 0: every element written, none read)."""
+    M, N, K, lda, ldb, ldc = 200, 300, 130, 136, 333, 301
+    rng = synth.rng(91)
+    Ast = rng.integers(-8, 9, (M, lda)).astype(np.float32)
+    Bst = rng.integers(-8, 9, (K, ldb)).astype(np.float32)
+    Cst = np.full((M, ldc), 7.0, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_SGEMM_F32, [g.a(Ast, R), g.a(Bst, R), g.a(Cst, W)],
+               jacc.jacc_sgemm_params_t(M, N, K, lda, ldb, ldc, mode, 0))
+    g.run(); g.destroy()
+    ref = oracle.sgemm_rows(np.ascontiguousarray(Ast[:, :K]), np.ascontiguousarray(Bst[:, :N]))
+    assert np.array_equal(Cst[:, :N].astype(np.float64), ref)          # integer inputs: exact
+    # (columns N..ldc-1 of a W buffer are undefined after execute: W args are
+    # not uploaded, include/jacc.h)
+    A0 = np.zeros((5, 0), np.float32); B0 = np.zeros((0, 7), np.float32); C0 = np.full((5, 7), 3.0, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A0, R), g.a(B0, R), g.a(C0, W)],
+               jacc.jacc_sgemm_params_t(5, 7, 0, 0, 7, 7, mode, 0))
+    g.run(); g.destroy()
+    assert np.all(C0 == 0.0)
+
+
+@pytest.mark.parametrize("mode", [J.JACC_SGEMM_FFMA, J.JACC_SGEMM_3XTF32], ids=["ffma", "3xtf32"])
 @pytest.mark.parametrize("shape", SG_SHAPES)
 def test_sgemm_gates(mode, shape):
     M, N, K = shape
