@@ -117,14 +117,20 @@ class ClockSampler:
 class Suite:
     """The per-rank jacc-suite task graph (device-resident or host-buffer form)."""
 
-    def __init__(self, torch, J, jacc, rank, world, comm_ptr, host_mode=False, sgemm_mode=0, flags=0):
-        from paper_1508_06791_b200.torch_glue import make_graph
+    def __init__(self, torch, J, jacc, rank, world, comm_ptr, host_mode=False, sgemm_mode=0, flags=0, p2p=False):
+        from paper_1508_06791_b200.torch_glue import make_graph, peer_setup, peer_tensor
         self.torch, self.J = torch, J
         self.rank, self.world = rank, world
         dev = torch.device("cuda", torch.cuda.current_device())
+        p2p = p2p and world > 1
+        if p2p:   # collectives over NVLink peer memory, fused into their producers (DESIGN R23)
+            flags |= J.JACC_GRAPH_P2P
+            comm_ptr = 0
         self.g, self.streams = make_graph(dev.index, n_streams=4, rank=rank, world=world, nccl_comm=comm_ptr,
                                           flags=flags)
         g = self.g
+        if p2p:
+            peer_setup(g, 64 << 20)
         R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
         self.tasks = {}     # name -> list of task ids
         self.units = {}     # name -> algorithmic bytes or flops per launch
@@ -204,7 +210,8 @@ class Suite:
         else:
             L = [put(pos[lo:hi]), empty((hi - lo, 4), torch.float32)]
             V = put(vel[lo:hi])
-            ALL = torch.empty((n5, 4), dtype=torch.float32, device=dev)   # DEVICE temp, never transferred
+            # DEVICE temp, never transferred; with P2P it lives in the symmetric window
+            ALL = peer_tensor(g, (n5, 4)) if p2p else torch.empty((n5, 4), dtype=torch.float32, device=dev)
             keep.append(ALL)
             for k in range(synth.CFG5_STEPS):
                 task("allgather_pos", J.JACC_OP_ALLGATHER, [g.a(L[k % 2], R, f32x4=True), g.a(ALL, W, f32x4=True)])
@@ -446,28 +453,77 @@ def cfg1_latency(torch, J, reps=200):
     return out
 
 
+def _p2p_probe(torch, J, dist, rank, world, red_dev="cuda"):
+    """Map the peers' windows and run one fused histogram -> allreduce; None
+    if it works on every rank, else the reason (then the run uses NCCL)."""
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph, peer_setup
+    err = None
+    try:
+        g, _ = make_graph(torch.cuda.current_device(), n_streams=1, rank=rank, world=world,
+                          flags=J.JACC_GRAPH_P2P)
+        peer_setup(g, 1 << 20)
+        keys = torch.full((4096,), rank, dtype=torch.int32, device="cuda")
+        bins = torch.zeros(256, dtype=torch.int32, device="cuda")
+        g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, J.JACC_READ), g.a(bins, J.JACC_WRITE)],
+                   jacc.jacc_hist_params_t(256))
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins, J.JACC_READWRITE)])
+        g.run()
+        want = torch.zeros(256, dtype=torch.int32)
+        want[:world] = 4096
+        if not torch.equal(bins.cpu(), want):
+            err = "p2p probe: wrong allreduce result"
+        g.destroy()
+    except Exception as exc:
+        err = f"p2p probe failed: {str(exc)[:200]}"
+    bad = torch.tensor([1 if err else 0], device=red_dev)
+    dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    if bad.item() and not err:
+        err = "p2p probe failed on another rank"
+    return err
+
+
 def run_jacc(args):
     import torch
     import torch.distributed as dist
     rank, local, world = dist_env()
-    torch.cuda.set_device(local)
+    # JACC_BENCH_SHARED_GPU=1 (testing only, never a bench number): every rank
+    # on cuda:0 with a gloo process group, collectives over the P2P windows --
+    # exercises the whole N>1 code path on a one-GPU box.
+    shared = os.environ.get("JACC_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        args.comm = "p2p"
+    red_dev = "cpu" if shared else "cuda"
+    torch.cuda.set_device(0 if shared else local)
     comm_ptr = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        from paper_1508_06791_b200.torch_glue import nccl_comm_ptr
-        dist.barrier()
-        comm_ptr = nccl_comm_ptr()
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            from paper_1508_06791_b200.torch_glue import nccl_comm_ptr
+            dist.barrier()
+            comm_ptr = nccl_comm_ptr()
     import paper_1508_06791_b200 as J
     from paper_1508_06791_b200 import jacc
     peaks = _peaks()
 
+    p2p_note = None
+    if world > 1 and args.comm == "p2p":
+        p2p_note = _p2p_probe(torch, J, dist, rank, world, red_dev)
+        if p2p_note:
+            args.comm = "nccl"   # every rank agrees (the probe's verdict is all-reduced)
     smode = J.JACC_SGEMM_3XTF32 if args.sgemm_mode == "3xtf32" else J.JACC_SGEMM_FFMA
     # device-resident timed region: one compute stream (every task of the
     # suite fills the GPU on its own, so out-of-order issue cannot shorten
     # the step, and a single stream keeps each task's CUDA-event duration
     # free of overlap with other tasks); copies/collectives keep their streams
+    # Plan replay (the action list captured once as a CUDA graph) so that
+    # the per-task events time the device, not the host's issue of each
+    # launch (at cfg1's 2^20 the kernels are shorter than their issue).
+    p2p = args.comm == "p2p"
     suite = Suite(torch, J, jacc, rank, world, comm_ptr, host_mode=False, sgemm_mode=smode,
-                  flags=J.JACC_GRAPH_SERIAL)
+                  flags=J.JACC_GRAPH_SERIAL | (J.JACC_GRAPH_REPLAY if args.replay else 0), p2p=p2p)
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")   # 256 MiB > 126 MB L2
     for _ in range(args.warmup):
         suite.timed_step(flush)
@@ -477,7 +533,7 @@ def run_jacc(args):
     times = []
     launches = 0
     ktimes = {}
-    with ClockSampler(local) as clk:
+    with ClockSampler(0 if shared else local) as clk:
         for _ in range(args.steps):
             times.append(suite.timed_step(flush))
             launches += suite.g.stats()["launches"]
@@ -486,7 +542,7 @@ def run_jacc(args):
     torch.cuda.synchronize()
     total_ms = sum(times)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -502,7 +558,7 @@ def run_jacc(args):
     # ---- e2e: the same graph through the C-ABI with HOST (pinned) buffers
     e2e = None
     if not args.no_e2e:
-        hs = Suite(torch, J, jacc, rank, world, comm_ptr, host_mode=True, sgemm_mode=smode)
+        hs = Suite(torch, J, jacc, rank, world, comm_ptr, host_mode=True, sgemm_mode=smode, p2p=p2p)
         hs.g.run()                      # warm-up (device copies allocated)
         if world > 1:
             dist.barrier()
@@ -515,7 +571,7 @@ def run_jacc(args):
         st = hs.g.stats()
         e_ms = statistics.mean(et) * 1e3
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            t = torch.tensor([e_ms], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(st["h2d_bytes"]),
@@ -539,8 +595,12 @@ def run_jacc(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth/, seeded numpy PCG64)",
             "config": {"workload": WORKLOAD, "l2": "flushed before every timed step (256 MiB device write)",
-                       "parallelism": f"spmd{world}: index/row/target shards, NCCL allreduce/allgather",
-                       "compute_streams": 1, "e2e_compute_streams": 4,
+                       "parallelism": f"spmd{world}: index/row/target shards" + (
+                           "" if world == 1 else
+                           ", allreduce/allgather fused into their producer kernels over NVLink peer memory"
+                           if p2p else ", NCCL allreduce/allgather"),
+                       "collectives": None if world == 1 else args.comm + (f" ({p2p_note})" if p2p_note else ""),
+                       "compute_streams": 1, "e2e_compute_streams": 4, "plan_replay": bool(args.replay),
                        "sgemm_mode": args.sgemm_mode},
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
             "e2e": e2e, "step_ms": times, "counted_copies_device_resident": {
@@ -570,6 +630,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sgemm-mode", choices=["3xtf32", "ffma"], default="3xtf32")
+    ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 collectives: fused NVLink peer-memory kernels (default) or NCCL calls")
+    ap.add_argument("--no-replay", dest="replay", action="store_false",
+                    help="issue every action from the host each step instead of replaying the captured plan")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

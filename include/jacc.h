@@ -44,8 +44,9 @@
 extern "C" {
 #endif
 
-#define JACC_ABI_VERSION 1
+#define JACC_ABI_VERSION 2
 #define JACC_MAX_STREAMS 8
+#define JACC_PEER_MAX 8     /* ranks of one NVLink/NVSwitch domain (JACC_GRAPH_P2P) */
 
 /* ------------------------------------------------------------ status codes */
 typedef enum jacc_status {
@@ -105,6 +106,22 @@ typedef enum jacc_dtype {
                                 same pass, bit-identical to the pair); the
                                 action list and counted copies are unchanged,
                                 both tasks report the fused kernel's time   */
+#define JACC_GRAPH_P2P 16u   /* collectives over NVLink peer memory instead of
+                                NCCL (reading R23): every rank maps the other
+                                ranks' symmetric window (jacc_peer_init /
+                                jacc_peer_connect) and the collective's data
+                                moves as plain stores into peer memory.  A
+                                collective task that directly follows the
+                                kernel producing its data is FUSED into that
+                                kernel (histogram -> allreduce(bins), reduce
+                                -> allreduce(out), N-body step ->
+                                allgather(pos_out)): each block pushes its
+                                results to the peers as it finishes them and
+                                the last block completes the exchange -- one
+                                kernel, no NCCL.  Other collective tasks run
+                                as standalone peer-memory kernels.  Every
+                                rank must build the same graph (SPMD), as for
+                                NCCL; no communicator is needed.            */
 
 /* -------------------------------------------------------------- ops */
 typedef enum jacc_op {
@@ -264,6 +281,16 @@ typedef struct jacc_config {
 
 typedef struct jacc_graph jacc_graph_t;
 
+/* Exported description of one rank's peer window (JACC_GRAPH_P2P): a CUDA
+ * IPC memory handle plus its size.  Opaque bytes for the caller, who moves
+ * them between ranks (e.g. torch.distributed.all_gather_object).           */
+typedef struct jacc_peer_handle {
+    unsigned char ipc[64];  /* cudaIpcMemHandle_t of the window base          */
+    uint64_t window_bytes;  /* identical on every rank                        */
+    int32_t rank;           /* the exporting rank                             */
+    int32_t device;         /* its CUDA ordinal (diagnostics only)            */
+} jacc_peer_handle_t;
+
 /* Counters of the LAST execute (as planned and issued), then cumulative
  * totals since create.  Verified against the oracle's transfer model in
  * the counted-copies tests.                             */
@@ -334,6 +361,32 @@ int jacc_buffer_invalidate(jacc_graph_t *g, const void *host_ptr);
 
 /* Implicit sync, then release the device copies, events and owned streams. */
 int jacc_graph_destroy(jacc_graph_t *g);
+
+/* ---- peer windows (JACC_GRAPH_P2P, reading R23) -------------------------
+ * Sequence on every rank: create (flags | JACC_GRAPH_P2P) -> jacc_peer_init
+ * -> exchange the handles -> jacc_peer_connect -> jacc_peer_alloc / add_task
+ * (same order on every rank) -> execute ...  A world-1 graph needs neither
+ * init nor connect (the first execute creates a local window).
+ *
+ * jacc_peer_init: cudaMalloc a zeroed window of window_bytes (0 -> 64 MiB;
+ * at least the 256 KiB flag header) on the graph's device and return its
+ * handle.  Errors: _STATE (not a P2P graph, or already initialised), _OOM,
+ * _CUDA.                                                                   */
+int jacc_peer_init(jacc_graph_t *g, size_t window_bytes, jacc_peer_handle_t *out);
+
+/* Map the other ranks' windows.  handles[q] is rank q's handle, n == world;
+ * handles[rank] must be this graph's own.  Errors: _STATE (no init, or
+ * already connected), _INVALID_ARG (n, rank order, window sizes differ),
+ * _CUDA (cudaIpcOpenMemHandle: the GPUs cannot reach each other).          */
+int jacc_peer_connect(jacc_graph_t *g, const jacc_peer_handle_t *handles, int n);
+
+/* Allocate `bytes` (256-byte aligned) of the window for the caller: a
+ * device buffer at the SAME offset on every rank, so peers can store into
+ * it.  A DEVICE argument that a P2P collective writes from other ranks (the
+ * receive buffer of an ALLGATHER, the buffer of a BROADCAST) must come from
+ * here.  Owned by the graph (freed by destroy).  Errors: _STATE (no window),
+ * _OOM (window full).                                                      */
+int jacc_peer_alloc(jacc_graph_t *g, size_t bytes, void **dptr);
 
 const char *jacc_status_string(int status);
 const char *jacc_last_error(void);   /* thread-local detail of the last error */

@@ -23,8 +23,15 @@
 //     into one block histogram, merged ONCE per block into global memory
 //     with 256 atomicAdds.
 // nbins in (256, 4096]: a plain shared-memory-atomics block histogram.
+//
+// JACC_GRAPH_P2P fusion (reading R23): when the graph's next task is the
+// allreduce of these bins, the same kernel finishes it -- the last block to
+// merge (grid ticket) pushes the local bins into every rank's window over
+// NVLink, waits for the other ranks' rows and sums them in rank order
+// (peer.cuh block_allreduce): one launch instead of histogram + NCCL.
 #include "common.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace jacc_k {
 namespace {
@@ -74,9 +81,10 @@ __device__ __forceinline__ void count_key(unsigned *sub_lane_w, int k, unsigned 
     atomicAdd(sub_lane_w + ((kk >> 2) << 5), 1u << ((kk & 3u) << 3));
 }
 
+template <bool kPeer>
 __global__ void __launch_bounds__(kBlock) hist256_kernel(const int4 *__restrict__ keys4, int64_t n4,
                                                          const int32_t *__restrict__ edge, int n_edge,
-                                                         int32_t *__restrict__ bins, int nbins) {
+                                                         int32_t *__restrict__ bins, int nbins, PeerOp pop) {
     extern __shared__ unsigned smem[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned *sub = smem + warp * kSubWords;
@@ -135,6 +143,8 @@ __global__ void __launch_bounds__(kBlock) hist256_kernel(const int4 *__restrict_
     __syncthreads();
     // merged once per block into the global @Atomic bins
     if (threadIdx.x < nbins && blockh[threadIdx.x]) atomicAdd(&bins[threadIdx.x], (int)blockh[threadIdx.x]);
+    if (kPeer && peer::grid_last(pop.ctx, pop.slot))   // every block's bins are in: allreduce them
+        peer::block_allreduce<int>(pop.ctx, pop.slot, (size_t)pop.off, bins, nbins);
 }
 
 // nbins in (256, 4096]: one shared 32-bit histogram per block, smem atomics.
@@ -158,11 +168,13 @@ __global__ void __launch_bounds__(256) hist_big_kernel(const int32_t *__restrict
 size_t histogram_ws_bytes(int64_t, int) { return 0; }
 
 cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbins, void *, const jacc_schedule_t *s,
-                          cudaStream_t st, int *launches) {
+                          cudaStream_t st, int *launches, const PeerOp *pop) {
+    if (pop && (n <= 0 || nbins > 256)) return cudaErrorInvalidValue;   // the runtime only fuses these
     if (n <= 0) return cudaSuccess;
     int grid, block;
     if (nbins <= 256) {
-        cudaError_t e = set_max_dyn_smem((const void *)hist256_kernel, kSmemBytes);
+        auto kern = pop ? hist256_kernel<true> : hist256_kernel<false>;
+        cudaError_t e = set_max_dyn_smem((const void *)kern, kSmemBytes);
         if (e != cudaSuccess) return e;
         // unaligned head keys go to the edge path together with the tail
         int64_t head = (int64_t)(((16 - ((uintptr_t)keys & 15)) & 15) / 4);
@@ -182,7 +194,8 @@ cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbi
         }
         const int32_t *edge = edge_head > 0 ? keys : keys + tail0;
         const int n_edge = (int)(edge_head > 0 ? edge_head : n - tail0);
-        hist256_kernel<<<grid, block, kSmemBytes, st>>>((const int4 *)(keys + head), n4, edge, n_edge, bins, nbins);
+        kern<<<grid, block, kSmemBytes, st>>>((const int4 *)(keys + head), n4, edge, n_edge, bins, nbins,
+                                              pop ? *pop : PeerOp{});
     } else {
         pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
         hist_big_kernel<<<grid, block, nbins * 4, st>>>(keys, n, bins, nbins);

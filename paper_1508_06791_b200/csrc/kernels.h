@@ -11,6 +11,22 @@
 
 namespace jacc_k {
 
+// JACC_GRAPH_P2P (peer.cuh): the windows of all ranks as mapped in this
+// process (base[rank] = the local window), and one collective task's slot +
+// window offset (allreduce: staging area; allgather / broadcast: receive
+// buffer).  Passed to kernels by value.
+struct PeerCtx {
+    char *base[JACC_PEER_MAX];
+    int rank, world;
+};
+struct PeerOp {
+    PeerCtx ctx;
+    int slot;
+    int64_t off;
+};
+constexpr size_t kPeerHeaderBytes = 256 * 1024;   // == peer::kHeaderBytes
+constexpr int kPeerSlots = 1024;                  // == peer::kSlots
+
 int sm_count();   // SMs of the current device (148 on B200), cached per device
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
 // thread-safe (graphs of different devices may launch from different threads)
@@ -25,7 +41,8 @@ cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,
 // out[0] += sum(x) (out pre-zeroed by the runtime for W)
 size_t reduce_ws_bytes(int64_t n);
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws,
-                           const jacc_schedule_t *s, cudaStream_t st, int *launches);
+                           const jacc_schedule_t *s, cudaStream_t st, int *launches,
+                           const PeerOp *allreduce = nullptr);  // fused allreduce(out)
 // the runtime's "merge" of vadd -> reduce: c = a + b, out[0] += sum(c)
 bool vadd_reduce_fusable(const float *a, const float *b, const float *c);
 cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n, float *out, void *ws,
@@ -34,7 +51,8 @@ cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n,
 // bins[k] += #{keys == k}
 size_t histogram_ws_bytes(int64_t n, int nbins);
 cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbins, void *ws,
-                          const jacc_schedule_t *s, cudaStream_t st, int *launches);
+                          const jacc_schedule_t *s, cudaStream_t st, int *launches,
+                          const PeerOp *allreduce = nullptr);   // fused allreduce(bins), nbins <= 256, n > 0
 
 // APARAPI Black-Scholes
 cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,
@@ -52,7 +70,14 @@ cudaError_t sgemm_f32(const float *A, const float *B, float *C, const jacc_sgemm
 size_t nbody_ws_bytes(int64_t n_src, int64_t n_tgt);
 cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, float4 *pos_out,
                            int64_t n_tgt, const jacc_nbody_params_t *p, void *ws,
-                           const jacc_schedule_t *s, cudaStream_t st, int *launches);
+                           const jacc_schedule_t *s, cudaStream_t st, int *launches,
+                           const PeerOp *allgather = nullptr);  // fused allgather(pos_out), n_tgt > 0
+
+// JACC_GRAPH_P2P standalone collectives (peer.cu)
+size_t peer_allreduce_stage_bytes(int64_t n, int esz, int world);
+cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, cudaStream_t st, int *launches);
+cudaError_t peer_allgather(const PeerOp &op, const void *send, int64_t bytes, cudaStream_t st, int *launches);
+cudaError_t peer_broadcast(const PeerOp &op, int root, int64_t bytes, cudaStream_t st, int *launches);
 
 // 2D convolution
 cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,

@@ -31,8 +31,15 @@
 //     adds the chunks in order and applies kick + drift;
 //   * the self term is included: x_j - x_i = 0 with eps2 > 0 contributes 0;
 //     padding sources (j >= n_src) have m = 0 at the origin (contribute 0).
+//   * JACC_GRAPH_P2P fusion (reading R23): when the graph's next task
+//     all-gathers pos_out, the finish kernel performs it -- every thread
+//     stores its target's new position into its own slot of every rank's
+//     gathered buffer over NVLink as soon as it is computed, and the last
+//     block waits until every rank's positions have arrived.  The all-gather
+//     costs no separate launch and its transfer overlaps the kick/drift.
 #include "common.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace jacc_k {
 namespace {
@@ -261,24 +268,51 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const fl
 }
 
 // ---- chunk sum (in chunk order) + kick + drift ---------------------------
+// kPeer: also the all-gather of pos_out into offset pop.off of every rank's
+// window (rank r's targets at [r n_tgt, (r+1) n_tgt)).  Receivers publish
+// "ready" first: this kernel runs after the step's partial kernel, the last
+// reader of the gathered buffer, and only reads its own slot of it.
+template <bool kPeer>
 __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restrict__ part, int nchunks,
                                                            const float4 *__restrict__ pos_src, int64_t tgt_offset,
                                                            float4 *__restrict__ vel, float4 *__restrict__ pos_out,
-                                                           int64_t n_tgt, float dt, float G) {
+                                                           int64_t n_tgt, float dt, float G, PeerOp pop) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tgt) return;
-    float4 a = part[t];
-    for (int c = 1; c < nchunks; ++c) {
-        const float4 b = part[(int64_t)c * n_tgt + t];
-        a.x += b.x; a.y += b.y; a.z += b.z;
+    uint64_t e = 0;
+    if (kPeer) {
+        e = peer::epoch(pop.ctx, pop.slot);
+        if (blockIdx.x == 0 && threadIdx.x == 0) peer::signal_all(pop.ctx, peer::kReadyOff, pop.slot, e);
     }
-    float4 v = vel[t];
-    v.x = fmaf(G * a.x, dt, v.x);
-    v.y = fmaf(G * a.y, dt, v.y);
-    v.z = fmaf(G * a.z, dt, v.z);
-    vel[t] = v;
-    const float4 p = pos_src[tgt_offset + t];
-    pos_out[t] = make_float4(fmaf(v.x, dt, p.x), fmaf(v.y, dt, p.y), fmaf(v.z, dt, p.z), p.w);
+    float4 np = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < n_tgt) {
+        float4 a = part[t];
+        for (int c = 1; c < nchunks; ++c) {
+            const float4 b = part[(int64_t)c * n_tgt + t];
+            a.x += b.x; a.y += b.y; a.z += b.z;
+        }
+        float4 v = vel[t];
+        v.x = fmaf(G * a.x, dt, v.x);
+        v.y = fmaf(G * a.y, dt, v.y);
+        v.z = fmaf(G * a.z, dt, v.z);
+        vel[t] = v;
+        const float4 p = pos_src[tgt_offset + t];
+        np = make_float4(fmaf(v.x, dt, p.x), fmaf(v.y, dt, p.y), fmaf(v.z, dt, p.z), p.w);
+        pos_out[t] = np;
+    }
+    if (!kPeer) return;
+    const PeerCtx &c = pop.ctx;
+    const size_t slot_off = (size_t)pop.off + ((size_t)c.rank * n_tgt + t) * sizeof(float4);
+    for (int k = 0; k < c.world; ++k) {
+        const int q = (c.rank + k) % c.world;   // local copy first, then the peers
+        if (q != c.rank) peer::block_wait(c, peer::kReadyOff, pop.slot, q, e);
+        if (t < n_tgt) *(float4 *)(c.base[q] + slot_off) = np;
+    }
+    if (!peer::grid_last(c, pop.slot)) return;
+    if (threadIdx.x == 0) {
+        peer::signal_all(c, peer::kDataOff, pop.slot, e);
+        *peer::count(c, pop.slot) = e;
+    }
+    if (threadIdx.x < (unsigned)c.world) peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, pop.slot, threadIdx.x), e);
 }
 
 typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
@@ -329,7 +363,8 @@ size_t nbody_ws_bytes(int64_t n_src, int64_t n_tgt) {
 
 cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, float4 *pos_out, int64_t n_tgt,
                            const jacc_nbody_params_t *p, void *ws, const jacc_schedule_t *, cudaStream_t st,
-                           int *launches) {
+                           int *launches, const PeerOp *pop) {
+    if (pop && n_tgt <= 0) return cudaErrorInvalidValue;   // the runtime only fuses n_tgt > 0
     if (n_tgt <= 0) return cudaSuccess;
     float4 *part = (float4 *)ws;
     const int64_t nchunks = (n_src + kChunk - 1) / kChunk;
@@ -344,9 +379,10 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
         v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);
         ++*launches;
     }
-    nbody_finish_kernel<<<(unsigned)((n_tgt + 255) / 256), 256, 0, st>>>(part, nchunks > 0 ? (int)nchunks : 1,
-                                                                         pos_src, p->tgt_offset, vel, pos_out, n_tgt,
-                                                                         p->dt, p->G);
+    auto fin = pop ? nbody_finish_kernel<true> : nbody_finish_kernel<false>;
+    fin<<<(unsigned)((n_tgt + 255) / 256), 256, 0, st>>>(part, nchunks > 0 ? (int)nchunks : 1, pos_src,
+                                                         p->tgt_offset, vel, pos_out, n_tgt, p->dt, p->G,
+                                                         pop ? *pop : PeerOp{});
     ++*launches;
     return cudaGetLastError();
 }

@@ -1,0 +1,145 @@
+// peer.cu -- standalone collective kernels over NVLink peer memory
+// (JACC_GRAPH_P2P; protocol and window layout in peer.cuh).  These serve the
+// collective tasks that are NOT fused into their producer kernel (the fused
+// forms live in histogram.cu, reduce.cu and nbody.cu):
+//   allreduce-sum (north_star: "NCCL allreduce of partial sums or bins"),
+//   all-gather ("N-body positions by NCCL all-gather over NVLink"),
+//   broadcast (SGEMM's replicated B).
+// Every rank's kernel both sends (stores into the peers' windows) and
+// receives (waits for the peers' data flags), so a task's completion event
+// means the result is in place on this rank, like the NCCL call it replaces.
+#include "common.cuh"
+#include "kernels.h"
+#include "peer.cuh"
+
+namespace jacc_k {
+namespace {
+
+constexpr int kBlock = 512;
+
+// n * world small enough for one block: push, signal, wait, sum in one CTA.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) allreduce_small_kernel(PeerCtx c, int slot, int64_t stage_off, T *buf,
+                                                                 int64_t n) {
+    peer::block_allreduce<T>(c, slot, (size_t)stage_off, buf, n);
+}
+
+// Large n, phase 1: every block pushes its slice of buf into row [rank] of
+// every rank's staging area (parity e & 1); the last block signals.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) allreduce_push_kernel(PeerCtx c, int slot, int64_t stage_off,
+                                                                const T *buf, int64_t n) {
+    const uint64_t e = peer::epoch(c, slot);
+    const size_t row = (size_t)n * sizeof(T), half = row * c.world;
+    const size_t mine = (size_t)stage_off + (e & 1) * half + (size_t)c.rank * row;
+    const size_t per = (row / gridDim.x + 15) & ~(size_t)15;   // 16-byte aligned slices
+    const size_t lo = per * blockIdx.x < row ? per * blockIdx.x : row;
+    const size_t hi = lo + per < row ? lo + per : row;
+    for (int q = 0; q < c.world; ++q)
+        peer::block_copy(c.base[q] + mine + lo, (const char *)buf + lo, hi - lo, threadIdx.x, blockDim.x);
+    if (peer::grid_last(c, slot) && threadIdx.x == 0) {
+        peer::signal_all(c, peer::kDataOff, slot, e);
+        *peer::count(c, slot) = e;
+    }
+}
+
+// Large n, phase 2 (same stream): wait for every rank, sum rows in rank order.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) allreduce_sum_kernel(PeerCtx c, int slot, int64_t stage_off, T *buf,
+                                                               int64_t n) {
+    const uint64_t e = *(volatile uint64_t *)peer::count(c, slot);   // bumped by phase 1
+    if (threadIdx.x < (unsigned)c.world) peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, threadIdx.x), e);
+    __syncthreads();
+    const T *rows = (const T *)(c.base[c.rank] + stage_off + (e & 1) * (size_t)n * c.world * sizeof(T));
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T acc = __ldcg(rows + i);
+        for (int q = 1; q < c.world; ++q) acc += __ldcg(rows + (size_t)q * n + i);
+        buf[i] = acc;
+    }
+}
+
+// All-gather (root < 0): rank r's `bytes` of src go to offset dst_off +
+// r * bytes of every rank's window (its own included).  Broadcast (root >=
+// 0): the root's src goes to offset dst_off of every other rank.  A rank
+// that receives first publishes "ready" (its destination is free: the task
+// runs after every local reader of it), a sender waits for the receiver's
+// ready before storing into it.
+__global__ void __launch_bounds__(kBlock) gather_kernel(PeerCtx c, int slot, const char *src, int64_t dst_off,
+                                                        int64_t bytes, int root) {
+    const uint64_t e = peer::epoch(c, slot);
+    const bool receives = root < 0 || c.rank != root;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && receives) peer::signal_all(c, peer::kReadyOff, slot, e);
+    const size_t per = ((size_t)bytes / gridDim.x + 15) & ~(size_t)15;
+    const size_t lo = per * blockIdx.x < (size_t)bytes ? per * blockIdx.x : (size_t)bytes;
+    const size_t hi = lo + per < (size_t)bytes ? lo + per : (size_t)bytes;
+    if (root < 0 || c.rank == root) {
+        const size_t seg = root < 0 ? (size_t)dst_off + (size_t)c.rank * bytes : (size_t)dst_off;
+        for (int k = 0; k < c.world; ++k) {
+            const int q = (c.rank + k) % c.world;    // start with the local copy
+            if (q == c.rank) {
+                if (root < 0) peer::block_copy(c.base[q] + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
+                continue;
+            }
+            peer::block_wait(c, peer::kReadyOff, slot, q, e);
+            peer::block_copy(c.base[q] + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
+        }
+    }
+    if (!peer::grid_last(c, slot)) return;
+    if (threadIdx.x == 0) {
+        peer::signal_all(c, peer::kDataOff, slot, e);
+        *peer::count(c, slot) = e;
+    }
+    if (root < 0) {
+        if (threadIdx.x < (unsigned)c.world)
+            peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, threadIdx.x), e);
+    } else if (threadIdx.x == 0 && c.rank != root) {
+        peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, root), e);
+    }
+}
+
+int copy_grid(int64_t bytes) {
+    // ~64 KiB per block, at most 32 blocks (a few SMs: the copy is NVLink-bound)
+    int64_t g = (bytes + (64 << 10) - 1) / (64 << 10);
+    return (int)(g < 1 ? 1 : g > 32 ? 32 : g);
+}
+
+}  // namespace
+
+size_t peer_allreduce_stage_bytes(int64_t n, int esz, int world) { return 2 * (size_t)n * esz * world; }
+
+cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, cudaStream_t st, int *launches) {
+    const int esz = 4;
+    if ((size_t)n * esz * op.ctx.world <= (64u << 10)) {
+        if (is_int)
+            allreduce_small_kernel<int><<<1, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (int *)buf, n);
+        else
+            allreduce_small_kernel<float><<<1, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (float *)buf, n);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    const int g = copy_grid(n * esz);
+    if (is_int) {
+        allreduce_push_kernel<int><<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (const int *)buf, n);
+        allreduce_sum_kernel<int><<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (int *)buf, n);
+    } else {
+        allreduce_push_kernel<float><<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (const float *)buf, n);
+        allreduce_sum_kernel<float><<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (float *)buf, n);
+    }
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t peer_allgather(const PeerOp &op, const void *send, int64_t bytes, cudaStream_t st, int *launches) {
+    gather_kernel<<<copy_grid(bytes), kBlock, 0, st>>>(op.ctx, op.slot, (const char *)send, op.off, bytes, -1);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t peer_broadcast(const PeerOp &op, int root, int64_t bytes, cudaStream_t st, int *launches) {
+    const char *src = op.ctx.base[op.ctx.rank] + op.off;
+    gather_kernel<<<copy_grid(bytes), kBlock, 0, st>>>(op.ctx, op.slot, src, op.off, bytes, root);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace jacc_k

@@ -13,8 +13,13 @@
 //      order and adds the total to out[0], then re-arms the ticket.
 // For a given n the grid is fixed, so the result is bitwise reproducible.
 // HBM-bound: 4 algorithmic bytes per element.
+//
+// JACC_GRAPH_P2P fusion (reading R23): when the next task is the allreduce
+// of out, the last block also completes it over NVLink peer memory (push the
+// local total to every rank, wait, sum the ranks' totals in rank order).
 #include "common.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace jacc_k {
 namespace {
@@ -37,11 +42,11 @@ __device__ __forceinline__ float block_sum(float v, float *sh) {
 // value is a[i] + b[i] (one fp32 add, exactly the vadd kernel's), stored to
 // c and summed in the very same order as reduce_kernel<false> on c -- so the
 // merged pair produces bit-identical c and s in one pass over a and b.
-template <bool kFused>
+template <bool kFused, bool kPeer>
 __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, const float *__restrict__ xb,
                                                         float *__restrict__ xc, int64_t n, int64_t head,
                                                         float *__restrict__ out, float *__restrict__ partials,
-                                                        unsigned *__restrict__ ticket) {
+                                                        unsigned *__restrict__ ticket, PeerOp pop) {
     __shared__ float sh[32];
     __shared__ bool last;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -93,6 +98,7 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
         out[0] += p;       // @Atomic ADD semantics: result += sum
         *ticket = 0u;      // re-arm for the next launch (stream-ordered)
     }
+    if (kPeer) peer::block_allreduce<float>(pop.ctx, pop.slot, (size_t)pop.off, out, 1);
 }
 
 }  // namespace
@@ -108,7 +114,7 @@ void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
 }  // namespace
 
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, const jacc_schedule_t *s,
-                           cudaStream_t st, int *launches) {
+                           cudaStream_t st, int *launches, const PeerOp *pop) {
     int grid, block;
     const int64_t head = (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4) < n
                              ? (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4)
@@ -116,7 +122,11 @@ cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, cons
     reduce_grid(n, s, &grid, &block);
     float *partials = (float *)ws;
     unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
-    reduce_kernel<false><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket);
+    if (pop)
+        reduce_kernel<false, true><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket, *pop);
+    else
+        reduce_kernel<false, false><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket,
+                                                            PeerOp{});
     ++*launches;
     return cudaGetLastError();
 }
@@ -132,7 +142,7 @@ cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n,
     reduce_grid(n, s_reduce, &grid, &block);
     float *partials = (float *)ws;
     unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
-    reduce_kernel<true><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket);
+    reduce_kernel<true, false><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket, PeerOp{});
     ++*launches;
     return cudaGetLastError();
 }

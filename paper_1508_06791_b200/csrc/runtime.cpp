@@ -84,6 +84,7 @@ struct Buffer {
     void *dptr = nullptr;   // graph-owned device copy (or == host for DEVICE)
     bool dev_current = false;  // device copy == host value at the end of the last execute
     bool invalidated = false;
+    bool in_window = false; // device copy lives in the P2P window (freed with it)
     cudaEvent_t ev_h2d = nullptr;
 };
 
@@ -108,6 +109,8 @@ struct Task {
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;   // timing
     cudaEvent_t ev_dep = nullptr;                       // dependency (no timing)
     float ms = 0.f;
+    int slot = -1;              // JACC_GRAPH_P2P: collective slot (peer.cuh)
+    int64_t peer_off = -1;      // JACC_GRAPH_P2P allreduce: staging offset in the window
 };
 
 enum ActKind { A_H2D, A_MEMSET0, A_KERNEL, A_COLLECTIVE, A_D2H };
@@ -146,6 +149,11 @@ struct jacc_graph {
     std::vector<cudaEvent_t> ev_join;
     bool capturing = false;          // issue() runs under stream capture
     bool last_was_replay = false;    // current execute = one graph launch on compute[0]
+    // JACC_GRAPH_P2P: symmetric window (peer.cuh) and the peers' mappings
+    char *win = nullptr;
+    size_t win_bytes = 0, win_top = 0;   // bump allocator (same sequence on every rank)
+    char *peer_base[JACC_PEER_MAX] = {};
+    bool peer_connected = false;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -154,6 +162,31 @@ namespace {
 int n_streams_of(const jacc_graph *g) {
     if (g->cfg.flags & (JACC_GRAPH_NAIVE | JACC_GRAPH_SERIAL)) return 1;
     return g->cfg.n_compute > 0 ? g->cfg.n_compute : 4;
+}
+
+bool p2p(const jacc_graph *g) { return g->cfg.flags & JACC_GRAPH_P2P; }
+
+// Bump-allocate from the P2P window (256-byte aligned); -1 when full.
+int64_t win_alloc(jacc_graph *g, size_t bytes) {
+    const size_t off = (g->win_top + 255) & ~(size_t)255;
+    if (!g->win || off + bytes > g->win_bytes) return -1;
+    g->win_top = off + (bytes ? bytes : 16);
+    return (int64_t)off;
+}
+
+// Offset of [p, p + bytes) inside the local window, or -1.
+int64_t win_off(const jacc_graph *g, const void *p, size_t bytes) {
+    const char *c = (const char *)p;
+    if (!g->win || c < g->win + jacc_k::kPeerHeaderBytes || c + bytes > g->win + g->win_bytes) return -1;
+    return (int64_t)(c - g->win);
+}
+
+jacc_k::PeerCtx peer_ctx(const jacc_graph *g) {
+    jacc_k::PeerCtx c{};
+    for (int q = 0; q < g->cfg.world; ++q) c.base[q] = q == g->cfg.rank ? g->win : g->peer_base[q];
+    c.rank = g->cfg.rank;
+    c.world = g->cfg.world;
+    return c;
 }
 
 int cuda_fail(cudaError_t e, const char *what) {
@@ -457,8 +490,10 @@ void make_plan(jacc_graph *g) {
         std::stable_sort(roots.begin(), roots.end(), [&](int x, int y) { return prio[x] > prio[y]; });
         for (int r = 0; r < (int)roots.size(); ++r) root_stream[roots[r]] = std::min(r, ns - 1);
     }
+    int next_slot = 0;   // JACC_GRAPH_P2P: collective tasks numbered in insertion order
     for (int t = 0; t < (int)g->tasks.size(); ++t) {
         Task &T = g->tasks[t];
+        T.slot = is_collective(T.op) ? next_slot++ : -1;
         if (naive || (g->cfg.flags & JACC_GRAPH_SERIAL)) {
             T.stream = 0;
         } else if (is_collective(T.op)) {
@@ -521,6 +556,8 @@ void plan_counts(const jacc_graph *g, jacc_stats_t *s) {
     }
 }
 
+int merge_partner(const jacc_graph *g, int i);
+
 std::string dump_text(const jacc_graph *g) {
     std::string out;
     char line[256];
@@ -555,6 +592,15 @@ std::string dump_text(const jacc_graph *g) {
         }
         out += line;
     }
+    if (p2p(g))   // JACC_GRAPH_P2P: collectives fused into their producer's kernel
+        for (size_t t = 0; t < g->tasks.size(); ++t) {
+            const int j = merge_partner(g, (int)t);
+            if (j >= 0 && is_collective(g->tasks[j].op)) {
+                snprintf(line, sizeof line, "fuse t%zu %s + t%d %s slot=%d\n", t, op_name(g->tasks[t].op), j,
+                         op_name(g->tasks[j].op), g->tasks[j].slot);
+                out += line;
+            }
+        }
     return out;
 }
 
@@ -590,7 +636,56 @@ cudaStream_t stream_of(jacc_graph *g, const Task &T) {
     return g->compute[T.stream % g->n_streams];
 }
 
+int peer_init_window(jacc_graph *g, size_t bytes);
+
+// JACC_GRAPH_P2P: give every collective task its window memory, before the
+// other device copies are allocated.  Allreduce: a staging area (2 epochs x
+// world rows).  Allgather / broadcast: the buffer the peers store into must
+// sit in the window at the same offset on every rank -- a graph-owned device
+// copy is allocated there, a DEVICE argument must come from jacc_peer_alloc.
+// Window offsets are handed out in task order, identical on every rank.
+int prepare_peer(jacc_graph *g) {
+    if (!g->win) {
+        if (g->cfg.world > 1) return fail(JACC_ERR_STATE, "P2P graph with world %d: jacc_peer_init/connect first",
+                                          g->cfg.world);
+        int rc = peer_init_window(g, 0);   // world 1: a local window
+        if (rc != JACC_OK) return rc;
+    }
+    if (g->cfg.world > 1 && !g->peer_connected) return fail(JACC_ERR_STATE, "P2P graph not connected");
+    for (Task &T : g->tasks) {
+        if (!is_collective(T.op)) continue;
+        if (T.slot >= jacc_k::kPeerSlots)
+            return fail(JACC_ERR_UNSUPPORTED, "P2P graph with more than %d collective tasks", jacc_k::kPeerSlots);
+        const TaskArg &a = T.args[0];
+        if (T.op == JACC_OP_ALLREDUCE_SUM) {
+            if (T.peer_off < 0) {
+                T.peer_off = win_alloc(g, jacc_k::peer_allreduce_stage_bytes((int64_t)a.count, 4, g->cfg.world));
+                if (T.peer_off < 0) return fail(JACC_ERR_OOM, "P2P window full (allreduce staging)");
+            }
+            continue;
+        }
+        Buffer &B = g->bufs[T.args[T.op == JACC_OP_ALLGATHER ? 1 : 0].buf];
+        if (B.device) {
+            if (win_off(g, B.dptr, B.bytes) < 0)
+                return fail(JACC_ERR_INVALID_ARG, "%s: DEVICE buffer %p is not in the P2P window (jacc_peer_alloc)",
+                            op_name(T.op), B.dptr);
+        } else if (!B.in_window) {
+            if (B.dptr) dev_free(g, B.dptr, B.bytes);   // allocated before it became a P2P receiver
+            const int64_t off = win_alloc(g, B.bytes);
+            if (off < 0) return fail(JACC_ERR_OOM, "P2P window full (%zu-byte buffer)", B.bytes);
+            B.dptr = g->win + off;
+            B.in_window = true;
+            B.dev_current = false;
+        }
+    }
+    return JACC_OK;
+}
+
 int prepare_memory(jacc_graph *g) {
+    if (p2p(g)) {
+        int rc = prepare_peer(g);
+        if (rc != JACC_OK) return rc;
+    }
     for (Buffer &B : g->bufs) {
         if (!B.device && !B.dptr) {
             B.dptr = dev_alloc(g, B.bytes);
@@ -639,7 +734,26 @@ int nccl_dtype(int dt, uint64_t count, uint64_t *n_out) {
     return dt == JACC_I32 ? jacc_nccl::kInt32 : jacc_nccl::kFloat32;
 }
 
-int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
+jacc_k::PeerOp peer_op(const jacc_graph *g, const Task &C) {
+    jacc_k::PeerOp op{};
+    op.ctx = peer_ctx(g);
+    op.slot = C.slot;
+    if (C.op == JACC_OP_ALLREDUCE_SUM) op.off = C.peer_off;
+    else {
+        const Buffer &B = g->bufs[C.args[C.op == JACC_OP_ALLGATHER ? 1 : 0].buf];
+        op.off = win_off(g, B.dptr, B.bytes);
+    }
+    return op;
+}
+
+// `fuse`: the collective task fused into this kernel (JACC_GRAPH_P2P), or NULL.
+int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Task *fuse = nullptr) {
+    jacc_k::PeerOp fop{};
+    const jacc_k::PeerOp *fp = nullptr;
+    if (fuse) {
+        fop = peer_op(g, *fuse);
+        fp = &fop;
+    }
     auto P = [&](int i) { return g->bufs[T.args[i].buf].dptr; };
     const jacc_schedule_t *sched = T.has_sched ? &T.sched : nullptr;
     const TaskArg *a = T.args.data();
@@ -651,12 +765,12 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
             break;
         case JACC_OP_REDUCE_SUM_F32:
             e = jacc_k::reduce_sum_f32((const float *)P(0), (int64_t)a[0].count, (float *)P(1), T.ws, sched, st,
-                                       launches);
+                                       launches, fp);
             break;
         case JACC_OP_HISTOGRAM_I32:
             e = jacc_k::histogram_i32((const int32_t *)P(0), (int64_t)a[0].count, (int32_t *)P(1),
                                       ((const jacc_hist_params_t *)T.params.data())->nbins, T.ws, sched, st,
-                                      launches);
+                                      launches, fp);
             break;
         case JACC_OP_BLACKSCHOLES_F32:
             e = jacc_k::blackscholes_f32((const float *)P(0), (float *)P(1), (float *)P(2), (int64_t)a[0].count,
@@ -674,7 +788,7 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
         case JACC_OP_NBODY_STEP_F32:
             e = jacc_k::nbody_step_f32((const float4 *)P(0), (int64_t)a[0].count, (float4 *)P(1), (float4 *)P(2),
                                        (int64_t)a[1].count, (const jacc_nbody_params_t *)T.params.data(), T.ws, sched,
-                                       st, launches);
+                                       st, launches, fp);
             break;
         case JACC_OP_CONV2D_F32: {
             const jacc_conv2d_params_t *cp = (const jacc_conv2d_params_t *)T.params.data();
@@ -696,6 +810,18 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
         case JACC_OP_ALLREDUCE_SUM:
         case JACC_OP_ALLGATHER:
         case JACC_OP_BROADCAST: {
+            if (p2p(g)) {   // over NVLink peer memory (peer.cu)
+                const jacc_k::PeerOp op = peer_op(g, T);
+                const int64_t bytes = (int64_t)(a[0].count * dtype_size(a[0].dtype));
+                if (T.op == JACC_OP_ALLREDUCE_SUM)
+                    e = jacc_k::peer_allreduce(op, P(0), (int64_t)a[0].count, a[0].dtype == JACC_I32, st, launches);
+                else if (T.op == JACC_OP_ALLGATHER)
+                    e = jacc_k::peer_allgather(op, P(0), bytes, st, launches);
+                else
+                    e = jacc_k::peer_broadcast(op, ((const jacc_bcast_params_t *)T.params.data())->root, bytes, st,
+                                               launches);
+                break;
+            }
             uint64_t n;
             int dt = nccl_dtype(a[0].dtype, a[0].count, &n);
             if (g->cfg.world == 1 && !g->cfg.nccl_comm) {
@@ -727,8 +853,33 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches) {
 // JACC_GRAPH_MERGE ("merge"): task i = vadd whose output c is the input
 // of task i + 1 = reduce, on the same stream, pointers 16-byte aligned ->
 // index of the reduce task to fuse with it, else -1.
+//
+// JACC_GRAPH_P2P (reading R23): task i produces exactly the data that task
+// i + 1, a collective, exchanges -> i + 1 is fused into task i's kernel:
+//   histogram(keys, bins) [nbins <= 256, n > 0] -> allreduce(bins)
+//   reduce(x, out)                              -> allreduce(out)
+//   nbody(src, vel, pos_out) [n_tgt > 0]        -> allgather(pos_out -> recv)
+int p2p_partner(const jacc_graph *g, int i) {
+    const int j = i + 1;
+    if (j >= (int)g->tasks.size()) return -1;
+    const Task &V = g->tasks[i], &C = g->tasks[j];
+    if (C.op == JACC_OP_ALLREDUCE_SUM && V.op == JACC_OP_HISTOGRAM_I32 && C.args[0].buf == V.args[1].buf &&
+        ((const jacc_hist_params_t *)V.params.data())->nbins <= 256 && V.args[0].count > 0)
+        return j;
+    if (C.op == JACC_OP_ALLREDUCE_SUM && V.op == JACC_OP_REDUCE_SUM_F32 && C.args[0].buf == V.args[1].buf) return j;
+    if (C.op == JACC_OP_ALLGATHER && V.op == JACC_OP_NBODY_STEP_F32 && C.args[0].buf == V.args[2].buf &&
+        V.args[1].count > 0)
+        return j;
+    return -1;
+}
+
 int merge_partner(const jacc_graph *g, int i) {
-    if (!(g->cfg.flags & JACC_GRAPH_MERGE) || (g->cfg.flags & JACC_GRAPH_NAIVE) || g->cfg.fail_task > 0) return -1;
+    if ((g->cfg.flags & JACC_GRAPH_NAIVE) || g->cfg.fail_task > 0) return -1;
+    if (p2p(g)) {
+        const int j = p2p_partner(g, i);
+        if (j >= 0) return j;
+    }
+    if (!(g->cfg.flags & JACC_GRAPH_MERGE)) return -1;
     const int j = i + 1;
     if (j >= (int)g->tasks.size()) return -1;
     const Task &V = g->tasks[i], &R = g->tasks[j];
@@ -791,7 +942,9 @@ int issue(jacc_graph *g) {
                 if (M.kind == A_MEMSET0 && (M.task == A.task || M.task == partner))
                     CK(cudaMemsetAsync(g->bufs[M.buf].dptr, 0, g->bufs[M.buf].bytes, st));
             int rc;
-            if (partner >= 0) {
+            if (partner >= 0 && is_collective(g->tasks[partner].op)) {   // P2P: collective fused into T's kernel
+                rc = launch_task(g, T, st, &launches, &g->tasks[partner]);
+            } else if (partner >= 0) {
                 const Task &Rt = g->tasks[partner];
                 auto P = [&](const Task &U, int i) { return g->bufs[U.args[i].buf].dptr; };
                 cudaError_t e = jacc_k::vadd_reduce_f32(
@@ -903,6 +1056,23 @@ int issue_replay(jacc_graph *g) {
     return JACC_OK;
 }
 
+int peer_init_window(jacc_graph *g, size_t bytes) {
+    if (bytes == 0) bytes = (size_t)64 << 20;
+    if (bytes < jacc_k::kPeerHeaderBytes + 4096) bytes = jacc_k::kPeerHeaderBytes + 4096;
+    int rc = ensure_resources(g);
+    if (rc != JACC_OK) return rc;
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(JACC_ERR_OOM, "P2P window of %zu bytes", bytes);
+    }
+    CK(cudaMemset(p, 0, bytes));   // flags, counts and tickets start at 0
+    g->win = (char *)p;
+    g->win_bytes = bytes;
+    g->win_top = jacc_k::kPeerHeaderBytes;
+    return JACC_OK;
+}
+
 }  // namespace
 
 // ================================================================ ABI
@@ -935,7 +1105,7 @@ size_t jacc_abi_sizeof(const char *name) {
 #define S(T) if (!strcmp(name, #T)) return sizeof(T)
     S(jacc_arg_t); S(jacc_schedule_t); S(jacc_config_t); S(jacc_stats_t);
     S(jacc_hist_params_t); S(jacc_sgemm_params_t); S(jacc_nbody_params_t); S(jacc_bcast_params_t);
-    S(jacc_conv2d_params_t); S(jacc_corr_params_t); S(jacc_spmv_params_t);
+    S(jacc_conv2d_params_t); S(jacc_corr_params_t); S(jacc_spmv_params_t); S(jacc_peer_handle_t);
 #undef S
     return 0;
 }
@@ -946,8 +1116,10 @@ int jacc_graph_create(jacc_graph_t **out, const jacc_config_t *cfg) {
         return fail(JACC_ERR_INVALID_ARG, "rank %d / world %d", cfg->rank, cfg->world);
     if (cfg->n_compute < 0 || cfg->n_compute > JACC_MAX_STREAMS)
         return fail(JACC_ERR_INVALID_ARG, "n_compute %d", cfg->n_compute);
-    if (cfg->world > 1 && !cfg->nccl_comm)
-        return fail(JACC_ERR_INVALID_ARG, "world > 1 needs an NCCL communicator");
+    if (cfg->world > 1 && !cfg->nccl_comm && !(cfg->flags & JACC_GRAPH_P2P))
+        return fail(JACC_ERR_INVALID_ARG, "world > 1 needs an NCCL communicator (or JACC_GRAPH_P2P)");
+    if ((cfg->flags & JACC_GRAPH_P2P) && cfg->world > JACC_PEER_MAX)
+        return fail(JACC_ERR_INVALID_ARG, "JACC_GRAPH_P2P: world %d > %d", cfg->world, JACC_PEER_MAX);
     if (cfg->device < 0) return fail(JACC_ERR_INVALID_ARG, "device %d", cfg->device);
     if ((cfg->alloc == nullptr) != (cfg->free == nullptr))
         return fail(JACC_ERR_INVALID_ARG, "alloc and free hooks come together");
@@ -1117,13 +1289,73 @@ int jacc_buffer_invalidate(jacc_graph_t *g, const void *host_ptr) {
     return fail(JACC_ERR_NOT_FOUND, "no host buffer at %p", host_ptr);
 }
 
+int jacc_peer_init(jacc_graph_t *g, size_t window_bytes, jacc_peer_handle_t *out) {
+    if (!g || !out) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (!(g->cfg.flags & JACC_GRAPH_P2P)) return fail(JACC_ERR_STATE, "not a JACC_GRAPH_P2P graph");
+    if (g->win) return fail(JACC_ERR_STATE, "peer window already initialised");
+    int rc = peer_init_window(g, window_bytes);
+    if (rc != JACC_OK) return rc;
+    memset(out, 0, sizeof *out);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, g->win));
+    static_assert(sizeof h <= sizeof out->ipc, "ipc handle size");
+    memcpy(out->ipc, &h, sizeof h);
+    out->window_bytes = g->win_bytes;
+    out->rank = g->cfg.rank;
+    out->device = g->cfg.device;
+    return JACC_OK;
+}
+
+int jacc_peer_connect(jacc_graph_t *g, const jacc_peer_handle_t *h, int n) {
+    if (!g || !h) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (!g->win) return fail(JACC_ERR_STATE, "jacc_peer_init first");
+    if (g->peer_connected) return fail(JACC_ERR_STATE, "already connected");
+    if (n != g->cfg.world) return fail(JACC_ERR_INVALID_ARG, "%d handles for world %d", n, g->cfg.world);
+    for (int q = 0; q < n; ++q) {
+        if (h[q].rank != q) return fail(JACC_ERR_INVALID_ARG, "handle %d is rank %d's", q, h[q].rank);
+        if (h[q].window_bytes != g->win_bytes)
+            return fail(JACC_ERR_INVALID_ARG, "window sizes differ (rank %d: %llu, here %zu)", q,
+                        (unsigned long long)h[q].window_bytes, g->win_bytes);
+    }
+    CK(cudaSetDevice(g->cfg.device));
+    for (int q = 0; q < n; ++q) {
+        if (q == g->cfg.rank) continue;
+        cudaIpcMemHandle_t ih;
+        memcpy(&ih, h[q].ipc, sizeof ih);
+        void *p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int k = 0; k < q; ++k)
+                if (g->peer_base[k]) { cudaIpcCloseMemHandle(g->peer_base[k]); g->peer_base[k] = nullptr; }
+            return cuda_fail(e, "cudaIpcOpenMemHandle (peer window)");
+        }
+        g->peer_base[q] = (char *)p;
+    }
+    g->peer_connected = true;
+    return JACC_OK;
+}
+
+int jacc_peer_alloc(jacc_graph_t *g, size_t bytes, void **dptr) {
+    if (!g || !dptr) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
+    if (!g->win) {
+        if (!(g->cfg.flags & JACC_GRAPH_P2P) || g->cfg.world > 1)
+            return fail(JACC_ERR_STATE, "no peer window (JACC_GRAPH_P2P + jacc_peer_init)");
+        int rc = peer_init_window(g, 0);
+        if (rc != JACC_OK) return rc;
+    }
+    const int64_t off = win_alloc(g, bytes);
+    if (off < 0) return fail(JACC_ERR_OOM, "P2P window full (%zu bytes requested)", bytes);
+    *dptr = g->win + off;
+    return JACC_OK;
+}
+
 int jacc_graph_destroy(jacc_graph_t *g) {
     if (!g) return JACC_OK;
     if (g->res_ready) {
         cudaSetDevice(g->cfg.device);
         sync_all(g);
         for (Buffer &B : g->bufs) {
-            if (!B.device) dev_free(g, B.dptr, B.bytes);
+            if (!B.device && !B.in_window) dev_free(g, B.dptr, B.bytes);
             if (B.ev_h2d) cudaEventDestroy(B.ev_h2d);
         }
         for (Task &T : g->tasks) {
@@ -1141,6 +1373,9 @@ int jacc_graph_destroy(jacc_graph_t *g) {
         if (g->ev_fork) cudaEventDestroy(g->ev_fork);
         for (cudaEvent_t e : g->ev_join) cudaEventDestroy(e);
     }
+    for (int q = 0; q < JACC_PEER_MAX; ++q)
+        if (g->peer_base[q]) cudaIpcCloseMemHandle(g->peer_base[q]);
+    if (g->win) cudaFree(g->win);
     delete g;
     return JACC_OK;
 }

@@ -31,8 +31,10 @@ JACC_OK, JACC_ERR_INVALID_ARG, JACC_ERR_STATE, JACC_ERR_ACCESS, JACC_ERR_ALIAS, 
 JACC_F32, JACC_I32, JACC_F32X4 = 1, 2, 3
 JACC_READ, JACC_WRITE, JACC_READWRITE = 1, 2, 3
 JACC_ARG_DEVICE, JACC_ARG_CACHABLE = 1, 2
-JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY, JACC_GRAPH_MERGE = 1, 2, 4, 8
+JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY, JACC_GRAPH_MERGE, JACC_GRAPH_P2P = 1, 2, 4, 8, 16
 JACC_MAX_STREAMS = 8
+JACC_PEER_MAX = 8
+JACC_ABI_VERSION = 2
 (JACC_OP_VADD_F32, JACC_OP_REDUCE_SUM_F32, JACC_OP_HISTOGRAM_I32, JACC_OP_BLACKSCHOLES_F32,
  JACC_OP_BLACKSCHOLES_SOA_F32, JACC_OP_SGEMM_F32, JACC_OP_NBODY_STEP_F32, JACC_OP_ALLREDUCE_SUM,
  JACC_OP_ALLGATHER, JACC_OP_BROADCAST, JACC_OP_CONV2D_F32, JACC_OP_CORR_POPC_U32,
@@ -111,7 +113,12 @@ class jacc_spmv_params_t(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("ncols", ctypes.c_int64)]
 
 
-STRUCTS = {"jacc_corr_params_t": jacc_corr_params_t, "jacc_spmv_params_t": jacc_spmv_params_t,
+class jacc_peer_handle_t(ctypes.Structure):
+    _fields_ = [("ipc", ctypes.c_ubyte * 64), ("window_bytes", ctypes.c_uint64), ("rank", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+STRUCTS = {"jacc_peer_handle_t": jacc_peer_handle_t, "jacc_corr_params_t": jacc_corr_params_t, "jacc_spmv_params_t": jacc_spmv_params_t,
            "jacc_arg_t": jacc_arg_t, "jacc_schedule_t": jacc_schedule_t, "jacc_config_t": jacc_config_t,
            "jacc_stats_t": jacc_stats_t, "jacc_hist_params_t": jacc_hist_params_t,
            "jacc_sgemm_params_t": jacc_sgemm_params_t, "jacc_nbody_params_t": jacc_nbody_params_t,
@@ -135,11 +142,14 @@ _lib.jacc_status_string.restype = ctypes.c_char_p
 _lib.jacc_last_error.restype = ctypes.c_char_p
 _lib.jacc_abi_sizeof.argtypes = [ctypes.c_char_p]
 _lib.jacc_abi_sizeof.restype = ctypes.c_size_t
+_lib.jacc_peer_init.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(jacc_peer_handle_t)]
+_lib.jacc_peer_connect.argtypes = [_vp, ctypes.POINTER(jacc_peer_handle_t), ctypes.c_int]
+_lib.jacc_peer_alloc.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
 
 EXPORTS = ["jacc_graph_create", "jacc_graph_add_task", "jacc_graph_execute", "jacc_graph_sync",
            "jacc_graph_stats", "jacc_graph_task_ms", "jacc_graph_dump", "jacc_buffer_invalidate",
            "jacc_graph_destroy", "jacc_status_string", "jacc_last_error", "jacc_abi_version",
-           "jacc_abi_sizeof"]
+           "jacc_abi_sizeof", "jacc_peer_init", "jacc_peer_connect", "jacc_peer_alloc"]
 
 jacc_graph_create = _lib.jacc_graph_create
 jacc_graph_add_task = _lib.jacc_graph_add_task
@@ -154,6 +164,12 @@ jacc_status_string = _lib.jacc_status_string
 jacc_last_error = _lib.jacc_last_error
 jacc_abi_version = _lib.jacc_abi_version
 jacc_abi_sizeof = _lib.jacc_abi_sizeof
+jacc_peer_init = _lib.jacc_peer_init
+jacc_peer_connect = _lib.jacc_peer_connect
+jacc_peer_alloc = _lib.jacc_peer_alloc
+
+if jacc_abi_version() != JACC_ABI_VERSION:
+    raise ImportError(f"{LIB_PATH}: ABI version {jacc_abi_version()} != binding's {JACC_ABI_VERSION} (rebuild)")
 
 
 class JaccError(RuntimeError):
@@ -273,6 +289,22 @@ class Graph:
         buf = ctypes.create_string_buffer(need.value)
         check(jacc_graph_dump(self._h, buf, need.value, ctypes.byref(need)), "jacc_graph_dump")
         return buf.value.decode()
+
+    # -- JACC_GRAPH_P2P peer windows (jacc_peer_init / _connect / _alloc) ----
+    def peer_init(self, window_bytes: int = 0) -> jacc_peer_handle_t:
+        h = jacc_peer_handle_t()
+        check(jacc_peer_init(self._h, int(window_bytes), ctypes.byref(h)), "jacc_peer_init")
+        return h
+
+    def peer_connect(self, handles) -> None:
+        arr = (jacc_peer_handle_t * len(handles))(*handles)
+        check(jacc_peer_connect(self._h, arr, len(handles)), "jacc_peer_connect")
+
+    def peer_alloc(self, nbytes: int) -> int:
+        """Device pointer of `nbytes` in the symmetric window (same offset on every rank)."""
+        p = ctypes.c_void_p()
+        check(jacc_peer_alloc(self._h, int(nbytes), ctypes.byref(p)), "jacc_peer_alloc")
+        return int(p.value)
 
     def invalidate(self, obj) -> None:
         ptr = obj.ctypes.data if isinstance(obj, np.ndarray) else obj.data_ptr()

@@ -43,7 +43,7 @@ def test_struct_layouts_match_library():
     for name, S in jacc.STRUCTS.items():
         assert ctypes.sizeof(S) == J.jacc_abi_sizeof(name.encode()), name
     assert J.jacc_abi_sizeof(b"nope") == 0
-    assert J.jacc_abi_version() == 1
+    assert J.jacc_abi_version() == 2
 
 
 def test_status_strings():
@@ -222,3 +222,56 @@ def test_independent_tasks_spread_over_streams():
     assert streams[0] != streams[1]
     assert streams[2] == streams[0] and streams[3] == streams[1]
     g.destroy()
+
+
+def test_p2p_create_and_window_state():
+    # JACC_GRAPH_P2P: world > 1 needs no NCCL communicator, but a window
+    g = J.Graph(rank=1, world=2, flags=J.JACC_GRAPH_P2P)
+    with pytest.raises(J.JaccError, match="STATE"):
+        g.peer_alloc(1024)                    # no jacc_peer_init yet
+    with pytest.raises(J.JaccError, match="STATE"):
+        g.peer_connect([jacc.jacc_peer_handle_t(), jacc.jacc_peer_handle_t()])
+    g.destroy()
+    with pytest.raises(J.JaccError, match="INVALID_ARG"):
+        J.Graph(world=9, flags=J.JACC_GRAPH_P2P)   # one NVLink domain: <= JACC_PEER_MAX ranks
+    g = J.Graph(flags=J.JACC_GRAPH_NAIVE)
+    with pytest.raises(J.JaccError, match="STATE"):
+        g.peer_init(0)                        # not a P2P graph
+    g.destroy()
+
+
+def _p2p_fusions(flags=0, world=2):
+    """Fusion lines of the dump of the bench's per-rank graph shape."""
+    n = 64
+    g = J.Graph(rank=0, world=world, flags=J.JACC_GRAPH_P2P | flags)
+    keys = np.zeros(1000, np.int32); bins = np.zeros(256, np.int32)
+    x = np.zeros(10, np.float32); s = np.zeros(1, np.float32)
+    big = np.zeros(600, np.int32); bins2 = np.zeros(300, np.int32)
+    L = [np.zeros((n // world, 4), np.float32) for _ in range(2)]
+    V = np.zeros((n // world, 4), np.float32)
+    ALL = np.zeros((n, 4), np.float32)
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, 1), g.a(bins, 2)], jacc.jacc_hist_params_t(256))
+    g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins, 3)])
+    g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, 1), g.a(s, 2)])
+    g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(s, 3)])
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, 1), g.a(bins2, 2)], jacc.jacc_hist_params_t(300))
+    g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins2, 3)])      # nbins > 256: not fused
+    g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(big, 3)])        # no producer: standalone
+    for k in range(3):
+        g.add_task(J.JACC_OP_ALLGATHER, [g.a(L[k % 2], 1, f32x4=True), g.a(ALL, 2, f32x4=True)])
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(ALL, 1, f32x4=True), g.a(V, 3, f32x4=True),
+                                               g.a(L[(k + 1) % 2], 2, f32x4=True)],
+                   jacc.jacc_nbody_params_t(0, 0.016, 0.01, 1.0))
+    d = g.dump()
+    g.destroy()
+    return [l for l in d.splitlines() if l.startswith("fuse")]
+
+
+def test_p2p_fusion_rule():
+    """Reading R23: a collective fused into the kernel that produces its data
+    (hist -> allreduce(bins), reduce -> allreduce(out), nbody ->
+    allgather(pos_out)); collectives get slots in insertion order."""
+    f = _p2p_fusions()
+    assert f == ["fuse t0 hist + t1 allreduce slot=0", "fuse t2 reduce + t3 allreduce slot=1",
+                 "fuse t8 nbody + t9 allgather slot=5", "fuse t10 nbody + t11 allgather slot=6"], f
+    assert _p2p_fusions(J.JACC_GRAPH_NAIVE) == []    # the naive lowering fuses nothing

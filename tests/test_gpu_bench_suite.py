@@ -29,10 +29,14 @@ def _np(t):
 @pytest.fixture(scope="module")
 def suite_outputs():
     outs = {}
-    for form, host, flags in (("device", False, J.JACC_GRAPH_SERIAL), ("host", True, 0)):
+    # "device" = the timed region's configuration (one stream, plan replay:
+    # the first execute captures the action list and launches the graph)
+    for form, host, flags in (("device", False, J.JACC_GRAPH_SERIAL | J.JACC_GRAPH_REPLAY), ("host", True, 0)):
         s = bench.Suite(torch, J, jacc, 0, 1, 0, host_mode=host, sgemm_mode=J.JACC_SGEMM_3XTF32, flags=flags)
         s.g.run()
         st = s.g.stats()
+        if form == "device":
+            assert st["graph_captures"] == 1, st
         outs[form] = ({k: _np(v).copy() for k, v in s.out.items()}, st)
         s.g.destroy()
         del s
