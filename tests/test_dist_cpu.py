@@ -84,6 +84,27 @@ def _worker(rank, world, port, q):
         st = g.stats()
         res["plan"] = (st["h2d_count"], st["d2h_count"], st["collectives"], st["kernels"])
         g.destroy()
+        # JACC_GRAPH_P2P (R23): the per-rank graphs of the same SPMD program
+        # must agree on every collective's slot and on which collectives are
+        # fused into their producers (the peer flags are matched by slot)
+        g = J.Graph(rank=rank, world=world, flags=J.JACC_GRAPH_P2P)
+        keys = np.zeros(1000 + rank, np.int32); bins = np.zeros(256, np.int32)
+        s1 = np.zeros(1, np.float32)
+        g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, 1), g.a(bins, 2)], jacc.jacc_hist_params_t(256))
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins, 3)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(np.zeros(10 + rank, np.float32), 1), g.a(s1, 2)])
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(s1, 3)])
+        for k in range(10):
+            g.add_task(J.JACC_OP_ALLGATHER, [g.a(L[k % 2], 1, True, f32x4=True),
+                                             jacc.arg(ALL.data_ptr(), n, J.JACC_F32X4, 2, J.JACC_ARG_DEVICE)])
+            g.add_task(J.JACC_OP_NBODY_STEP_F32, [jacc.arg(ALL.data_ptr(), n, J.JACC_F32X4, 1, J.JACC_ARG_DEVICE),
+                                                   g.a(Vl, 3, True, f32x4=True), g.a(L[(k + 1) % 2], 2, True, f32x4=True)],
+                       jacc.jacc_nbody_params_t(lo, 0.016, 0.01, 1.0))
+        fuse = [l for l in g.dump().splitlines() if l.startswith("fuse")]
+        g.destroy()
+        every = [None] * world
+        dist.all_gather_object(every, fuse)
+        res["p2p_fuse"] = (len(fuse), all(f == fuse for f in every))
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, res))
@@ -107,6 +128,8 @@ def test_spmd_world2_gloo():
         assert "error" not in out[r], out[r].get("error")
         assert out[r]["hist"] and out[r]["reduce"] and out[r]["sgemm"] and out[r]["nbody"], out[r]
         assert out[r]["plan"] == (2, 3, 10, 10), out[r]["plan"]
+        # hist+allreduce, reduce+allreduce, 9 nbody+allgather (the first allgather has no producer)
+        assert out[r]["p2p_fuse"] == (11, True), out[r]["p2p_fuse"]
 
 
 def test_shard_range_partition():
