@@ -399,7 +399,9 @@ def cfg1_latency(torch, J, reps=200):
     a, b = synth.vadd_inputs()
     out = {}
     modes = {"direct": 0, "replay": J.JACC_GRAPH_REPLAY, "merge_replay": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY,
-             "e2e_direct": 0, "e2e_merge": J.JACC_GRAPH_MERGE}
+             "merge_replay_notiming": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING,
+             "e2e_direct": 0, "e2e_merge": J.JACC_GRAPH_MERGE,
+             "e2e_merge_replay_notiming": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING}
     for mode, flags in modes.items():
         host = mode.startswith("e2e")
         g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=flags)
@@ -437,7 +439,9 @@ def cfg1_latency(torch, J, reps=200):
     out["warm_copies"] = [int(st["h2d_count"]), int(st["d2h_count"])]
     g.destroy()
     K = 300
-    for mode, flags in {"kiter": 0, "kiter_merge_replay": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY}.items():
+    for mode, flags in {"kiter": 0, "kiter_merge_replay": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY,
+                        "kiter_merge_replay_notiming": J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY |
+                        J.JACC_GRAPH_NO_TIMING}.items():
         g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=flags)
         for _ in range(K):
             g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R), g.a(tb, R), g.a(tc, W)])

@@ -106,6 +106,10 @@ typedef enum jacc_dtype {
                                 same pass, bit-identical to the pair); the
                                 action list and counted copies are unchanged,
                                 both tasks report the fused kernel's time   */
+#define JACC_GRAPH_NO_TIMING 32u /* no per-task timing events (jacc_graph_task_ms
+                                then fails with _STATE): for many-task graphs
+                                whose cost is the events, e.g. the paper's
+                                K-iteration protocol            */
 #define JACC_GRAPH_P2P 16u   /* collectives over NVLink peer memory instead of
                                 NCCL (reading R23): every rank maps the other
                                 ranks' symmetric window (jacc_peer_init /

@@ -40,13 +40,15 @@ cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,
 
 // out[0] += sum(x) (out pre-zeroed by the runtime for W)
 size_t reduce_ws_bytes(int64_t n);
+// assign: out[0] = sum (W output, no memset) instead of out[0] += sum
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws,
-                           const jacc_schedule_t *s, cudaStream_t st, int *launches,
+                           const jacc_schedule_t *s, cudaStream_t st, int *launches, bool assign = false,
                            const PeerOp *allreduce = nullptr);  // fused allreduce(out)
 // the runtime's "merge" of vadd -> reduce: c = a + b, out[0] += sum(c)
 bool vadd_reduce_fusable(const float *a, const float *b, const float *c);
 cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n, float *out, void *ws,
-                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches);
+                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches, bool assign = false,
+                            const PeerOp *allreduce = nullptr);
 
 // bins[k] += #{keys == k}
 size_t histogram_ws_bytes(int64_t n, int nbins);

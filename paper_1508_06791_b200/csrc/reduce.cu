@@ -46,7 +46,7 @@ template <bool kFused, bool kPeer>
 __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, const float *__restrict__ xb,
                                                         float *__restrict__ xc, int64_t n, int64_t head,
                                                         float *__restrict__ out, float *__restrict__ partials,
-                                                        unsigned *__restrict__ ticket, PeerOp pop) {
+                                                        unsigned *__restrict__ ticket, int assign, PeerOp pop) {
     __shared__ float sh[32];
     __shared__ bool last;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) p += __ldcg(partials + b);
     p = block_sum(p, sh);
     if (threadIdx.x == 0) {
-        out[0] += p;       // @Atomic ADD semantics: result += sum
+        // @Atomic ADD semantics: result += sum; a W output is
+        // auto-zeroed, i.e. result = 0 + sum -- stored directly
+        out[0] = assign ? 0.f + p : out[0] + p;
         *ticket = 0u;      // re-arm for the next launch (stream-ordered)
     }
     if (kPeer) peer::block_allreduce<float>(pop.ctx, pop.slot, (size_t)pop.off, out, 1);
@@ -114,7 +116,7 @@ void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
 }  // namespace
 
 cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, const jacc_schedule_t *s,
-                           cudaStream_t st, int *launches, const PeerOp *pop) {
+                           cudaStream_t st, int *launches, bool assign, const PeerOp *pop) {
     int grid, block;
     const int64_t head = (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4) < n
                              ? (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / 4)
@@ -123,10 +125,11 @@ cudaError_t reduce_sum_f32(const float *x, int64_t n, float *out, void *ws, cons
     float *partials = (float *)ws;
     unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
     if (pop)
-        reduce_kernel<false, true><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket, *pop);
+        reduce_kernel<false, true><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket,
+                                                           assign, *pop);
     else
         reduce_kernel<false, false><<<grid, block, 0, st>>>(x, nullptr, nullptr, n, head, out, partials, ticket,
-                                                            PeerOp{});
+                                                            assign, PeerOp{});
     ++*launches;
     return cudaGetLastError();
 }
@@ -137,12 +140,16 @@ bool vadd_reduce_fusable(const float *a, const float *b, const float *c) {
 
 // c = a + b and out[0] += sum(c) in one pass (requires vadd_reduce_fusable).
 cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n, float *out, void *ws,
-                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches) {
+                            const jacc_schedule_t *s_reduce, cudaStream_t st, int *launches, bool assign,
+                            const PeerOp *pop) {
     int grid, block;
     reduce_grid(n, s_reduce, &grid, &block);
     float *partials = (float *)ws;
     unsigned *ticket = (unsigned *)((char *)ws + sizeof(float) * kMaxGrid);
-    reduce_kernel<true, false><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket, PeerOp{});
+    if (pop)
+        reduce_kernel<true, true><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket, assign, *pop);
+    else
+        reduce_kernel<true, false><<<grid, block, 0, st>>>(a, b, c, n, 0, out, partials, ticket, assign, PeerOp{});
     ++*launches;
     return cudaGetLastError();
 }

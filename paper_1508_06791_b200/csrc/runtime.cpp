@@ -110,6 +110,7 @@ struct Task {
     cudaEvent_t ev_dep = nullptr;                       // dependency (no timing)
     float ms = 0.f;
     int slot = -1;              // JACC_GRAPH_P2P: collective slot (peer.cuh)
+    int fused_into = -1;        // issue: task whose kernel also runs this one (merge), else -1
     int64_t peer_off = -1;      // JACC_GRAPH_P2P allreduce: staging offset in the window
 };
 
@@ -130,6 +131,9 @@ struct jacc_graph {
     std::vector<Action> plan;
     std::vector<int> last_writer;
     bool planned = false;
+    std::vector<char> plan_dev_valid;   // residency the plan was made for (re-plan when it changes)
+    std::vector<std::vector<int>> memset_bufs;   // per task: its MEMSET0 buffers (from the plan)
+    std::vector<int> h2d_order;         // plan indices of the H2D actions, critical path first
     bool have_times = false;
     // resources
     bool res_ready = false;
@@ -460,15 +464,21 @@ std::vector<int> h2d_issue_order(const jacc_graph *g) {
 // ------------------------------------------------------------- planner
 // Transfer model G.3 (reading R3) -- identical to the
 // oracle's oracle/graph_model.py:plan, which tests/ compare against.
+std::vector<char> initial_dev_valid(const jacc_graph *g) {
+    std::vector<char> v(g->bufs.size());
+    for (size_t b = 0; b < g->bufs.size(); ++b) {
+        const Buffer &B = g->bufs[b];
+        v[b] = (B.cachable && B.dev_current && !B.invalidated && B.dptr) ? 1 : 0;
+    }
+    return v;
+}
+
 void make_plan(jacc_graph *g) {
     const bool naive = g->cfg.flags & JACC_GRAPH_NAIVE;
     const int nb = (int)g->bufs.size();
-    std::vector<char> dev_valid(nb), host_valid(nb, 1);
+    std::vector<char> dev_valid = initial_dev_valid(g), host_valid(nb, 1);
+    g->plan_dev_valid = dev_valid;
     g->last_writer.assign(nb, -1);
-    for (int b = 0; b < nb; ++b) {
-        const Buffer &B = g->bufs[b];
-        dev_valid[b] = (B.cachable && B.dev_current && !B.invalidated && B.dptr) ? 1 : 0;
-    }
     g->plan.clear();
     // streams (out-of-order issue, R6): a task with predecessors stays on the
     // stream of its latest one (a chain needs no cross-stream waits); a root
@@ -539,7 +549,16 @@ void make_plan(jacc_graph *g) {
         });
         for (int b : stale) g->plan.push_back({A_D2H, b, g->last_writer[b]});
     }
+    g->memset_bufs.assign(g->tasks.size(), {});
+    for (const Action &A : g->plan)
+        if (A.kind == A_MEMSET0) g->memset_bufs[A.task].push_back(A.buf);
+    g->h2d_order = h2d_issue_order(g);
     g->planned = true;
+}
+
+// Re-plan only when a task was added or the residency the plan assumed changed.
+void ensure_plan(jacc_graph *g) {
+    if (!g->planned || g->plan_dev_valid != initial_dev_valid(g)) make_plan(g);
 }
 
 void plan_counts(const jacc_graph *g, jacc_stats_t *s) {
@@ -631,7 +650,9 @@ int ensure_resources(jacc_graph *g) {
     return JACC_OK;
 }
 
+// The stream a task's work is issued on (a merged task: its host kernel's).
 cudaStream_t stream_of(jacc_graph *g, const Task &T) {
+    if (T.fused_into >= 0) return stream_of(g, g->tasks[T.fused_into]);
     if (T.stream < 0) return g->comm;
     return g->compute[T.stream % g->n_streams];
 }
@@ -695,8 +716,10 @@ int prepare_memory(jacc_graph *g) {
         if (!B.ev_h2d) CK(cudaEventCreateWithFlags(&B.ev_h2d, cudaEventDisableTiming));
     }
     for (Task &T : g->tasks) {
-        if (!T.ev_start) CK(cudaEventCreate(&T.ev_start));
-        if (!T.ev_end) CK(cudaEventCreate(&T.ev_end));
+        if (!(g->cfg.flags & JACC_GRAPH_NO_TIMING)) {
+            if (!T.ev_start) CK(cudaEventCreate(&T.ev_start));
+            if (!T.ev_end) CK(cudaEventCreate(&T.ev_end));
+        }
         if (!T.ev_dep) CK(cudaEventCreateWithFlags(&T.ev_dep, cudaEventDisableTiming));
         size_t need = 0;
         const TaskArg *a = T.args.data();
@@ -747,7 +770,9 @@ jacc_k::PeerOp peer_op(const jacc_graph *g, const Task &C) {
 }
 
 // `fuse`: the collective task fused into this kernel (JACC_GRAPH_P2P), or NULL.
-int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Task *fuse = nullptr) {
+// `assign`: a REDUCE's W output was not memset; its kernel stores the sum.
+int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Task *fuse = nullptr,
+                bool assign = false) {
     jacc_k::PeerOp fop{};
     const jacc_k::PeerOp *fp = nullptr;
     if (fuse) {
@@ -765,7 +790,7 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
             break;
         case JACC_OP_REDUCE_SUM_F32:
             e = jacc_k::reduce_sum_f32((const float *)P(0), (int64_t)a[0].count, (float *)P(1), T.ws, sched, st,
-                                       launches, fp);
+                                       launches, assign, fp);
             break;
         case JACC_OP_HISTOGRAM_I32:
             e = jacc_k::histogram_i32((const int32_t *)P(0), (int64_t)a[0].count, (int32_t *)P(1),
@@ -889,15 +914,53 @@ int merge_partner(const jacc_graph *g, int i) {
     return jacc_k::vadd_reduce_fusable(P(V, 0), P(V, 1), P(V, 2)) ? j : -1;
 }
 
+// The tasks issued as one kernel with task i (i first): i alone, a merged
+// vadd -> reduce pair, a P2P producer -> collective pair, or the triple
+// vadd -> reduce -> allreduce (MERGE + P2P).
+std::vector<int> fused_group(const jacc_graph *g, int i) {
+    std::vector<int> grp{i};
+    const int j = merge_partner(g, i);
+    if (j < 0) return grp;
+    grp.push_back(j);
+    if (!is_collective(g->tasks[j].op) && p2p(g) && g->cfg.fail_task == 0) {
+        const int k = p2p_partner(g, j);
+        if (k >= 0) grp.push_back(k);
+    }
+    return grp;
+}
+
 int issue(jacc_graph *g) {
-    const int nb = (int)g->bufs.size();
+    const int nb = (int)g->bufs.size(), nt = (int)g->tasks.size();
     std::vector<char> h2d_issued(nb, 0);
-    std::vector<char> task_done(g->tasks.size(), 0);
+    std::vector<char> task_done(nt, 0);
     int launches = 0;
     jacc_stats_t &S = g->stats;
     const bool naive = g->cfg.flags & JACC_GRAPH_NAIVE;
+    const bool timing = !(g->cfg.flags & JACC_GRAPH_NO_TIMING);
+    // pre-pass: kernel groups (merges), then which tasks' dependency events
+    // some other stream waits on -- only those are recorded
+    std::vector<std::vector<int>> group(nt);
+    for (Task &T : g->tasks) T.fused_into = -1;
+    for (const Action &A : g->plan) {
+        if ((A.kind != A_KERNEL && A.kind != A_COLLECTIVE) || g->tasks[A.task].fused_into >= 0 ||
+            !group[A.task].empty())
+            continue;
+        group[A.task] = fused_group(g, A.task);
+        for (size_t k = 1; k < group[A.task].size(); ++k) g->tasks[group[A.task][k]].fused_into = A.task;
+    }
+    std::vector<char> need_dep(nt, 0);
+    for (int t = 0; t < nt; ++t) {
+        if (group[t].empty()) continue;
+        cudaStream_t st = stream_of(g, g->tasks[t]);
+        for (int u : group[t])
+            for (int p : g->tasks[u].preds)
+                if (g->tasks[p].fused_into != t && p != t && stream_of(g, g->tasks[p]) != st) need_dep[p] = 1;
+    }
+    for (const Action &A : g->plan)
+        if (A.kind == A_D2H && stream_of(g, g->tasks[A.task]) != g->d2h) need_dep[A.task] = 1;
+
     if (!naive) {   // all H2D first, critical path first; kernels wait on their own events
-        for (int i : h2d_issue_order(g)) {
+        for (int i : g->h2d_order) {
             Buffer &B = g->bufs[g->plan[i].buf];
             CK(cudaMemcpyAsync(B.dptr, (const void *)B.host, B.bytes, cudaMemcpyHostToDevice, g->h2d));
             CK(cudaEventRecord(B.ev_h2d, g->h2d));
@@ -918,47 +981,52 @@ int issue(jacc_graph *g) {
             if (g->cfg.fail_task > 0 && A.task == g->cfg.fail_task - 1)
                 return fail(JACC_ERR_INJECTED, "failure injected at task %d", A.task);
             cudaStream_t st = stream_of(g, T);
-            const int partner = merge_partner(g, A.task);   // -1, or the reduce task fused with it
+            const std::vector<int> &grp = group[A.task];
             // timing events: under CUDA-graph capture they must be EXTERNAL
             // record nodes (a plain record is only a capture dependency)
             auto rec = [&](cudaEvent_t e) {
                 return g->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
             };
-            for (int t : {A.task, partner}) {
-                if (t < 0) continue;
+            for (int t : grp) {
                 const Task &U = g->tasks[t];
                 for (const TaskArg &a : U.args)
                     if (h2d_issued[a.buf] && g->h2d != st) CK(cudaStreamWaitEvent(st, g->bufs[a.buf].ev_h2d, 0));
                 for (int p : U.preds) {
                     const Task &Pt = g->tasks[p];
-                    if (p != A.task && stream_of(g, Pt) != st) CK(cudaStreamWaitEvent(st, Pt.ev_dep, 0));
+                    if (p != A.task && Pt.fused_into != A.task && stream_of(g, Pt) != st)
+                        CK(cudaStreamWaitEvent(st, Pt.ev_dep, 0));
                 }
             }
-            CK(rec(T.ev_start));
-            if (partner >= 0) CK(rec(g->tasks[partner].ev_start));
-            // MEMSET0 actions (auto-zero of @Atomic outputs) of this task
-            // and of a merged partner (they sit just before its KERNEL action)
-            for (const Action &M : g->plan)
-                if (M.kind == A_MEMSET0 && (M.task == A.task || M.task == partner))
-                    CK(cudaMemsetAsync(g->bufs[M.buf].dptr, 0, g->bufs[M.buf].bytes, st));
+            if (timing)
+                for (int t : grp) CK(rec(g->tasks[t].ev_start));
+            // MEMSET0 actions (auto-zero of @Atomic outputs) of the
+            // group's tasks; a reduction's single float is instead assigned
+            // (not added) by its kernel -- one memset node less per task
+            bool assign = false;
+            for (int t : grp)
+                for (int b : g->memset_bufs[t]) {
+                    if (g->tasks[t].op == JACC_OP_REDUCE_SUM_F32) { assign = true; continue; }
+                    CK(cudaMemsetAsync(g->bufs[b].dptr, 0, g->bufs[b].bytes, st));
+                }
             int rc;
-            if (partner >= 0 && is_collective(g->tasks[partner].op)) {   // P2P: collective fused into T's kernel
-                rc = launch_task(g, T, st, &launches, &g->tasks[partner]);
-            } else if (partner >= 0) {
-                const Task &Rt = g->tasks[partner];
+            const Task *coll = grp.size() > 1 && is_collective(g->tasks[grp.back()].op) ? &g->tasks[grp.back()] : nullptr;
+            if (grp.size() > 1 && g->tasks[grp[1]].op == JACC_OP_REDUCE_SUM_F32 && T.op == JACC_OP_VADD_F32) {
+                const Task &Rt = g->tasks[grp[1]];
                 auto P = [&](const Task &U, int i) { return g->bufs[U.args[i].buf].dptr; };
+                jacc_k::PeerOp op{};
+                if (coll) op = peer_op(g, *coll);
                 cudaError_t e = jacc_k::vadd_reduce_f32(
                     (const float *)P(T, 0), (const float *)P(T, 1), (float *)P(T, 2), (int64_t)T.args[0].count,
-                    (float *)P(Rt, 1), Rt.ws, Rt.has_sched ? &Rt.sched : nullptr, st, &launches);
+                    (float *)P(Rt, 1), Rt.ws, Rt.has_sched ? &Rt.sched : nullptr, st, &launches, assign,
+                    coll ? &op : nullptr);
                 rc = e == cudaSuccess ? JACC_OK : fail(JACC_ERR_CUDA, "launch vadd+reduce: %s", cudaGetErrorString(e));
             } else {
-                rc = launch_task(g, T, st, &launches);
+                rc = launch_task(g, T, st, &launches, coll, assign);
             }
             if (rc != JACC_OK) return rc;
-            for (int t : {A.task, partner}) {
-                if (t < 0) continue;
-                CK(rec(g->tasks[t].ev_end));
-                CK(cudaEventRecord(g->tasks[t].ev_dep, st));   // cross-stream dependency marker
+            for (int t : grp) {
+                if (timing) CK(rec(g->tasks[t].ev_end));
+                if (need_dep[t]) CK(cudaEventRecord(g->tasks[t].ev_dep, st));   // cross-stream dependency marker
                 task_done[t] = 1;
             }
         } else if (A.kind == A_D2H) {
@@ -1179,10 +1247,11 @@ int jacc_graph_add_task(jacc_graph_t *g, jacc_op_t op, const jacc_arg_t *args, i
 int jacc_graph_execute(jacc_graph_t *g) {
     if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
     if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is already executing");
-    make_plan(g);
+    ensure_plan(g);
     int rc = ensure_resources(g);
     if (rc == JACC_OK) rc = prepare_memory(g);
     if (rc != JACC_OK) { g->state = ST_FAILED; return rc; }
+    ensure_plan(g);   // a device copy (re)allocated just now is not resident
     plan_counts(g, &g->stats);
     g->have_times = false;
     g->state = ST_EXECUTING;
@@ -1215,11 +1284,13 @@ int jacc_graph_sync(jacc_graph_t *g) {
         g->pending_error = rc;
         return rc;
     }
-    for (Task &T : g->tasks) {
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, T.ev_start, T.ev_end) == cudaSuccess) T.ms = ms;
+    if (!(g->cfg.flags & JACC_GRAPH_NO_TIMING)) {
+        for (Task &T : g->tasks) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, T.ev_start, T.ev_end) == cudaSuccess) T.ms = ms;
+        }
+        g->have_times = true;
     }
-    g->have_times = true;
     for (Buffer &B : g->bufs) {
         if (!B.device) {
             B.dev_current = true;
@@ -1257,6 +1328,7 @@ int jacc_graph_stats(const jacc_graph_t *g, jacc_stats_t *out) {
 int jacc_graph_task_ms(const jacc_graph_t *g, int task_id, float *ms) {
     if (!g || !ms) return fail(JACC_ERR_INVALID_ARG, "NULL argument");
     if (task_id < 0 || task_id >= (int)g->tasks.size()) return fail(JACC_ERR_NOT_FOUND, "task %d", task_id);
+    if (g->cfg.flags & JACC_GRAPH_NO_TIMING) return fail(JACC_ERR_STATE, "graph created with JACC_GRAPH_NO_TIMING");
     if (!g->have_times) return fail(JACC_ERR_STATE, "no completed execute");
     *ms = g->tasks[task_id].ms;
     return JACC_OK;

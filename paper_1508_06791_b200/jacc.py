@@ -32,6 +32,7 @@ JACC_F32, JACC_I32, JACC_F32X4 = 1, 2, 3
 JACC_READ, JACC_WRITE, JACC_READWRITE = 1, 2, 3
 JACC_ARG_DEVICE, JACC_ARG_CACHABLE = 1, 2
 JACC_GRAPH_NAIVE, JACC_GRAPH_SERIAL, JACC_GRAPH_REPLAY, JACC_GRAPH_MERGE, JACC_GRAPH_P2P = 1, 2, 4, 8, 16
+JACC_GRAPH_NO_TIMING = 32
 JACC_MAX_STREAMS = 8
 JACC_PEER_MAX = 8
 JACC_ABI_VERSION = 2

@@ -56,13 +56,15 @@ def test_cfg1_counted_copies_and_values():
     g.destroy()
 
 
-@pytest.mark.parametrize("flags", [0, "merge_replay"])
+@pytest.mark.parametrize("flags", [0, "merge_replay", "merge_replay_notiming"])
 def test_cfg1_k_iterations_one_graph(flags):
     """Paper protocol (SURVEY §8(c)-G row 'cfg1 xK'): K iterations of
     vadd -> reduce in ONE graph cost a single H2D per input and a single D2H
     per output (naive: 3K / 2K), and the final values equal one iteration's."""
     if flags == "merge_replay":
         flags = J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY
+    elif flags == "merge_replay_notiming":
+        flags = J.JACC_GRAPH_MERGE | J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING
     n, K = 1 << 16, 40
     a, b = synth.vadd_inputs(n, seed=5)
     c = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
@@ -81,6 +83,11 @@ def test_cfg1_k_iterations_one_graph(flags):
         assert np.array_equal(c, ref_c)
         ref, absum = oracle.reduce_sum(ref_c)
         assert abs(s[0] - ref) <= 1e-4 * absum
+    if flags & J.JACC_GRAPH_NO_TIMING:
+        with pytest.raises(J.JaccError, match="STATE"):
+            g.task_ms(0)
+    else:
+        assert g.task_ms(2 * K - 1) > 0
     g.destroy()
     gn = _graph(flags=J.JACC_GRAPH_NAIVE)
     for _ in range(K):
@@ -308,3 +315,47 @@ def test_merge_vadd_reduce_bit_identical(extra):
     assert np.array_equal(c0, oracle.vadd(a, b))
     assert (st1["h2d_count"], st1["d2h_count"]) == (st0["h2d_count"], st0["d2h_count"])
     assert st0["launches"] == 2 and st1["launches"] == 1
+
+
+def test_reduce_rw_accumulates_w_assigns():
+    """@Atomic semantics: W auto-zeroes (the kernel stores the
+    sum, no memset node), RW adds to the host value -- bitwise the sum + the
+    prior value, whichever path."""
+    x = synth.uniform_f32(70001, 9)
+    ref = None
+    for access, init in ((W, 123.0), (RW, 0.0), (RW, 5.5)):
+        s = np.full(1, init, np.float32)
+        g = _graph()
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(x, R), g.a(s, access)])
+        g.run()
+        st = g.stats()
+        assert st["memsets"] == (1 if access == W else 0)
+        g.destroy()
+        if ref is None:
+            ref = s[0]
+            r, absum = oracle.reduce_sum(x)
+            assert abs(ref - r) <= 1e-4 * absum
+        else:
+            assert s[0] == np.float32(init) + ref     # one fp32 add of the same tree sum
+
+
+def test_merge_p2p_triple_one_launch():
+    """MERGE + P2P at world 1: vadd -> reduce -> allreduce(s) is ONE kernel
+    (the fused vadd+reduce finishes the allreduce over the peer window), with
+    results bitwise equal to the unmerged graph."""
+    n = (1 << 20) + 40
+    a, b = synth.vadd_inputs(n, seed=23)
+    outs = {}
+    for flags in (0, J.JACC_GRAPH_MERGE | J.JACC_GRAPH_P2P):
+        c = np.zeros(n, np.float32); s = np.zeros(1, np.float32)
+        g = _graph(flags=flags)
+        g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+        g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(c, R), g.a(s, W)])
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(s, RW)])
+        for _ in range(3):
+            g.run()
+        outs[flags] = (c.copy(), s.copy(), g.stats())
+        g.destroy()
+    (c0, s0, st0), (c1, s1, st1) = outs.values()
+    assert np.array_equal(c0, c1) and np.array_equal(s0, s1)
+    assert st1["launches"] == 1 and st1["collectives"] == 1, st1
