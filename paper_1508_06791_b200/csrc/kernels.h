@@ -17,6 +17,7 @@ namespace jacc_k {
 // buffer).  Passed to kernels by value.
 struct PeerCtx {
     char *base[JACC_PEER_MAX];
+    char *self;   // == base[rank]: device code never indexes base[] with a runtime value
     int rank, world;
 };
 struct PeerOp {

@@ -17,7 +17,7 @@ namespace {
 
 constexpr int kBlock = 512;
 
-// n * world small enough for one block: push, signal, wait, sum in one CTA.
+// n small enough for one block: the flag-in-data exchange of peer.cuh.
 template <typename T>
 __global__ void __launch_bounds__(kBlock) allreduce_small_kernel(PeerCtx c, int slot, int64_t stage_off, T *buf,
                                                                  int64_t n) {
@@ -35,12 +35,10 @@ __global__ void __launch_bounds__(kBlock) allreduce_push_kernel(PeerCtx c, int s
     const size_t per = (row / gridDim.x + 15) & ~(size_t)15;   // 16-byte aligned slices
     const size_t lo = per * blockIdx.x < row ? per * blockIdx.x : row;
     const size_t hi = lo + per < row ? lo + per : row;
-    for (int q = 0; q < c.world; ++q)
-        peer::block_copy(c.base[q] + mine + lo, (const char *)buf + lo, hi - lo, threadIdx.x, blockDim.x);
-    if (peer::grid_last(c, slot) && threadIdx.x == 0) {
-        peer::signal_all(c, peer::kDataOff, slot, e);
-        *peer::count(c, slot) = e;
-    }
+    peer::for_each_rank(c, [&](int, char *b) {
+        peer::block_copy(b + mine + lo, (const char *)buf + lo, hi - lo, threadIdx.x, blockDim.x);
+    });
+    if (peer::grid_last(c, slot) && threadIdx.x == 0) peer::publish_data(c, slot, e);
 }
 
 // Large n, phase 2 (same stream): wait for every rank, sum rows in rank order.
@@ -48,9 +46,9 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock) allreduce_sum_kernel(PeerCtx c, int slot, int64_t stage_off, T *buf,
                                                                int64_t n) {
     const uint64_t e = *(volatile uint64_t *)peer::count(c, slot);   // bumped by phase 1
-    if (threadIdx.x < (unsigned)c.world) peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, threadIdx.x), e);
+    peer::wait_all_data(c, slot, e);
     __syncthreads();
-    const T *rows = (const T *)(c.base[c.rank] + stage_off + (e & 1) * (size_t)n * c.world * sizeof(T));
+    const T *rows = (const T *)(c.self + stage_off + (e & 1) * (size_t)n * c.world * sizeof(T));
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         T acc = __ldcg(rows + i);
         for (int q = 1; q < c.world; ++q) acc += __ldcg(rows + (size_t)q * n + i);
@@ -74,27 +72,19 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(PeerCtx c, int slot, con
     const size_t hi = lo + per < (size_t)bytes ? lo + per : (size_t)bytes;
     if (root < 0 || c.rank == root) {
         const size_t seg = root < 0 ? (size_t)dst_off + (size_t)c.rank * bytes : (size_t)dst_off;
-        for (int k = 0; k < c.world; ++k) {
-            const int q = (c.rank + k) % c.world;    // start with the local copy
+        peer::for_each_rank(c, [&](int q, char *b) {
             if (q == c.rank) {
-                if (root < 0) peer::block_copy(c.base[q] + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
-                continue;
+                if (root < 0) peer::block_copy(b + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
+                return;
             }
             peer::block_wait(c, peer::kReadyOff, slot, q, e);
-            peer::block_copy(c.base[q] + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
-        }
+            peer::block_copy(b + seg + lo, src + lo, hi - lo, threadIdx.x, blockDim.x);
+        });
     }
     if (!peer::grid_last(c, slot)) return;
-    if (threadIdx.x == 0) {
-        peer::signal_all(c, peer::kDataOff, slot, e);
-        *peer::count(c, slot) = e;
-    }
-    if (root < 0) {
-        if (threadIdx.x < (unsigned)c.world)
-            peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, threadIdx.x), e);
-    } else if (threadIdx.x == 0 && c.rank != root) {
-        peer::wait_ge(peer::flag(c.base[c.rank], peer::kDataOff, slot, root), e);
-    }
+    if (threadIdx.x == 0) peer::publish_data(c, slot, e);
+    if (root < 0) peer::wait_all_data(c, slot, e);
+    else if (threadIdx.x == 0 && c.rank != root) peer::wait_ge(peer::flag(c.self, peer::kDataOff, slot, root), e);
 }
 
 int copy_grid(int64_t bytes) {
@@ -105,11 +95,11 @@ int copy_grid(int64_t bytes) {
 
 }  // namespace
 
-size_t peer_allreduce_stage_bytes(int64_t n, int esz, int world) { return 2 * (size_t)n * esz * world; }
+size_t peer_allreduce_stage_bytes(int64_t n, int, int world) { return peer::allreduce_stage_bytes(n, world); }
 
 cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, cudaStream_t st, int *launches) {
     const int esz = 4;
-    if ((size_t)n * esz * op.ctx.world <= (64u << 10)) {
+    if (n <= 8192) {
         if (is_int)
             allreduce_small_kernel<int><<<1, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (int *)buf, n);
         else
@@ -136,7 +126,7 @@ cudaError_t peer_allgather(const PeerOp &op, const void *send, int64_t bytes, cu
 }
 
 cudaError_t peer_broadcast(const PeerOp &op, int root, int64_t bytes, cudaStream_t st, int *launches) {
-    const char *src = op.ctx.base[op.ctx.rank] + op.off;
+    const char *src = op.ctx.self + op.off;
     gather_kernel<<<copy_grid(bytes), kBlock, 0, st>>>(op.ctx, op.slot, src, op.off, bytes, root);
     ++*launches;
     return cudaGetLastError();

@@ -188,6 +188,7 @@ int64_t win_off(const jacc_graph *g, const void *p, size_t bytes) {
 jacc_k::PeerCtx peer_ctx(const jacc_graph *g) {
     jacc_k::PeerCtx c{};
     for (int q = 0; q < g->cfg.world; ++q) c.base[q] = q == g->cfg.rank ? g->win : g->peer_base[q];
+    c.self = g->win;
     c.rank = g->cfg.rank;
     c.world = g->cfg.world;
     return c;

@@ -27,16 +27,19 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--mode", default="3xtf32")
     ap.add_argument("--shards", type=int, default=1, help="nbody: time rank 0's target shard of N/shards bodies")
+    ap.add_argument("--p2p", action="store_true",
+                    help="hist/reduce/nbody: follow the op with its collective (allreduce / allgather) in a "
+                         "JACC_GRAPH_P2P graph at world 1, so the collective is fused into the op's kernel")
     a = ap.parse_args()
     import torch
     import paper_1508_06791_b200 as J
     from paper_1508_06791_b200 import jacc
-    from paper_1508_06791_b200.torch_glue import make_graph
+    from paper_1508_06791_b200.torch_glue import make_graph, peer_tensor
     R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
     dev = torch.device("cuda", 0)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     for op in a.ops:
-        g, _ = make_graph(0, n_streams=1)
+        g, _ = make_graph(0, n_streams=1, flags=J.JACC_GRAPH_P2P if a.p2p else 0)
         keep = []
 
         def D(x):
@@ -50,13 +53,18 @@ def main():
             units, kind = 12 * n, "GB/s"
         elif op == "reduce":
             n = a.n or synth.CFG1_N
-            g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(D(synth.uniform_f32(n, 1)), R),
-                                                   g.a(D(np.zeros(1, np.float32)), W)])
+            out = D(np.zeros(1, np.float32))
+            g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(D(synth.uniform_f32(n, 1)), R), g.a(out, W)])
+            if a.p2p:
+                g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(out, RW)])
             units, kind = 4 * n, "GB/s"
         elif op == "hist":
             n = a.n or synth.CFG2_N
-            g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(D(synth.hist_keys(n)), R), g.a(D(np.zeros(256, np.int32)), W)],
+            bins = D(np.zeros(256, np.int32))
+            g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(D(synth.hist_keys(n)), R), g.a(bins, W)],
                        jacc.jacc_hist_params_t(256))
+            if a.p2p:
+                g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins, RW)])
             units, kind = 4 * n, "GB/s"
         elif op == "bs":
             n = a.n or synth.CFG3_N
@@ -74,9 +82,12 @@ def main():
             n = a.n or synth.CFG5_N
             pos, vel = synth.nbody_state(n)
             lo, hi = synth.shard_range(n, 0, a.shards)
+            pout = D(np.zeros_like(pos[lo:hi]))
             g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(D(pos), R, f32x4=True), g.a(D(vel[lo:hi]), RW, f32x4=True),
-                                                   g.a(D(np.zeros_like(pos[lo:hi])), W, f32x4=True)],
+                                                   g.a(pout, W, f32x4=True)],
                        jacc.jacc_nbody_params_t(lo, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+            if a.p2p:
+                g.add_task(J.JACC_OP_ALLGATHER, [g.a(pout, R, f32x4=True), g.a(peer_tensor(g, (hi - lo, 4)), W, f32x4=True)])
             units, kind = 20 * n * (hi - lo), "TFLOP/s"
         elif op == "conv2d":
             n = a.n or 2048
