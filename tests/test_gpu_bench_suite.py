@@ -94,3 +94,75 @@ def test_suite_cfg5_invariants(suite_outputs):
     vmax = np.max(np.linalg.norm(vel[:, :3], axis=1))
     disp = np.linalg.norm(pos[:, :3] - pos0[:, :3].astype(np.float64), axis=1)
     assert np.all(np.isfinite(pos)) and np.max(disp) <= vmax * synth.CFG5_STEPS * synth.NBODY_DT * 1.0001
+
+
+# ------------------------------------------------------------------ world 2
+def _suite_worker(rank, world, port, q):
+    """One rank of the bench's N>1 graph (P2P collectives, the timed launch
+    configuration), both ranks on the box's one GPU."""
+    try:
+        import os
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path.insert(0, root)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        import paper_1508_06791_b200 as J
+        from paper_1508_06791_b200 import jacc
+        s = bench.Suite(torch, J, jacc, rank, world, 0, host_mode=False, sgemm_mode=J.JACC_SGEMM_3XTF32,
+                        flags=J.JACC_GRAPH_SERIAL | J.JACC_GRAPH_REPLAY, p2p=True)
+        for _ in range(2):      # capture, then replay (the N-body state advances: keep the first)
+            s.g.run()
+            if _ == 0:
+                out = {k: (v.cpu().numpy() if v.is_cuda else v.numpy()).copy() for k, v in s.out.items()}
+        st = s.g.stats()
+        s.g.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, {"out": out, "replays": int(st["graph_replays"])}))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+@pytest.mark.slow
+def test_suite_world2_p2p(suite_outputs):
+    """The bench's N = 2 graph at full size: every rank's shard against the
+    oracle (histogram and all-reduced bins bitwise, sums within tolerance)
+    and bitwise against the 1-GPU suite where the decomposition promises it
+    (vadd, Black-Scholes, SGEMM rows, N-body after 10 all-gathered steps)."""
+    import os
+    import torch.multiprocessing as mp
+    world = 2
+    port = 29900 + (os.getpid() % 90)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_suite_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    one, _ = suite_outputs["device"]
+    keys = synth.hist_keys()
+    bins_ref = oracle.histogram(keys, 256)
+    a, b = synth.vadd_inputs()
+    ref_s, absum = oracle.reduce_sum(oracle.vadd(a, b))
+    for r in range(world):
+        assert "error" not in res[r], res[r].get("error")
+        o = res[r]["out"]
+        assert res[r]["replays"] == 1
+        assert np.array_equal(o["bins"], bins_ref)                       # allreduce of the shards' bins
+        assert abs(float(o["s"][0]) - ref_s) <= 1e-4 * absum             # allreduce of partial sums
+        lo, hi = synth.shard_range(synth.CFG1_N, r, world)
+        assert np.array_equal(o["c"], one["c"][lo:hi])
+        lo, hi = synth.shard_range(synth.CFG3_N, r, world)
+        assert np.array_equal(o["call"], one["call"][lo:hi]) and np.array_equal(o["put"], one["put"][lo:hi])
+        lo, hi = synth.shard_range(synth.CFG4_MNK, r, world)
+        assert np.array_equal(o["C"], one["C"][lo:hi])
+        lo, hi = synth.shard_range(synth.CFG5_N, r, world)
+        assert np.array_equal(o["pos"], one["pos"][lo:hi]) and np.array_equal(o["vel"], one["vel"][lo:hi])
