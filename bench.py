@@ -129,8 +129,13 @@ class Suite:
         self.g, self.streams = make_graph(dev.index, n_streams=4, rank=rank, world=world, nccl_comm=comm_ptr,
                                           flags=flags)
         g = self.g
+        # e2e at N > 1: each rank copies only its 1/N row block of SGEMM's B
+        # over PCIe and the ranks all-gather B over NVLink,
+        # instead of every rank copying all 256 MiB through its own PCIe link
+        n4 = synth.CFG4_MNK
+        gather_b = host_mode and world > 1 and n4 % world == 0
         if p2p:
-            peer_setup(g, 64 << 20)
+            peer_setup(g, ((n4 * n4 * 4) if gather_b else 0) + (64 << 20))
         R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
         self.tasks = {}     # name -> list of task ids
         self.units = {}     # name -> algorithmic bytes or flops per launch
@@ -189,7 +194,15 @@ class Suite:
         n4 = synth.CFG4_MNK
         lo, hi = synth.shard_range(n4, rank, world)
         A, B = synth.sgemm_inputs(n4, n4, n4)
-        dA, dB = put(A[lo:hi]), put(B)
+        dA = put(A[lo:hi])
+        if gather_b:
+            klo, khi = synth.shard_range(n4, rank, world)
+            dBs = put(B[klo:khi])
+            dB = peer_tensor(g, (n4, n4)) if p2p else torch.empty((n4, n4), dtype=torch.float32, device=dev)
+            keep.append(dB)
+            task("allgather_B", J.JACC_OP_ALLGATHER, [g.a(dBs, R), g.a(dB, W)])
+        else:
+            dB = put(B)
         del A, B
         dC = empty((hi - lo, n4), torch.float32)
         task("sgemm", J.JACC_OP_SGEMM_F32, [g.a(dA, R), g.a(dB, R), g.a(dC, W)],

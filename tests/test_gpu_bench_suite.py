@@ -121,9 +121,19 @@ def _suite_worker(rank, world, port, q):
                 out = {k: (v.cpu().numpy() if v.is_cuda else v.numpy()).copy() for k, v in s.out.items()}
         st = s.g.stats()
         s.g.destroy()
+        del s
+        torch.cuda.empty_cache()
+        # the e2e (host-buffer) form: B copied in as 1/world row blocks and
+        # all-gathered over the peer windows before the SGEMM
+        h = bench.Suite(torch, J, jacc, rank, world, 0, host_mode=True, sgemm_mode=J.JACC_SGEMM_3XTF32, p2p=True)
+        h.g.run()
+        hst = h.g.stats()
+        hout = {k: (v.cpu().numpy() if v.is_cuda else v.numpy()).copy() for k, v in h.out.items()}
+        h.g.destroy()
         dist.barrier()
         dist.destroy_process_group()
-        q.put((rank, {"out": out, "replays": int(st["graph_replays"])}))
+        q.put((rank, {"out": out, "replays": int(st["graph_replays"]), "host_out": hout,
+                      "host_h2d_bytes": int(hst["h2d_bytes"]), "host_tasks": sorted(h.tasks)}))
     except Exception:
         import traceback
         q.put((rank, {"error": traceback.format_exc()}))
@@ -166,3 +176,15 @@ def test_suite_world2_p2p(suite_outputs):
         assert np.array_equal(o["C"], one["C"][lo:hi])
         lo, hi = synth.shard_range(synth.CFG5_N, r, world)
         assert np.array_equal(o["pos"], one["pos"][lo:hi]) and np.array_equal(o["vel"], one["vel"][lo:hi])
+        # host-buffer form: the same results, B arriving by all-gather
+        assert "allgather_B" in res[r]["host_tasks"]
+        for k in o:
+            assert np.array_equal(res[r]["host_out"][k], o[k]), k
+        # H2D per rank = its shards only: a, b, keys, u, A rows, B ROWS (not all of B), positions, velocities
+        def span(n):
+            l, h = synth.shard_range(n, r, world)
+            return h - l
+        n4 = synth.CFG4_MNK
+        want = (2 * 4 * span(synth.CFG1_N) + 4 * span(synth.CFG2_N) + 4 * span(synth.CFG3_N) +
+                4 * span(n4) * n4 * 2 + 16 * span(synth.CFG5_N) * 2)
+        assert res[r]["host_h2d_bytes"] == want, (res[r]["host_h2d_bytes"], want)
