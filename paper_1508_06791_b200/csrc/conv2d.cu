@@ -10,13 +10,132 @@
 // the (2r+1)^2 filter lives in registers; each thread produces a column of 4
 // outputs and slides a (4 + 2r)-tall register window over the tile, so every
 // shared-memory value it loads feeds up to (2r+1) FMAs.
+//
+// TMA path (row stride a multiple of 16 bytes, radius 2 = the paper's 5 x 5):
+// persistent blocks walk 64 x 64 output tiles in row-major order; the 72 x
+// (64 + 2r) input box of each tile (x from x0 - 4, y from y0 - r) arrives by
+// one cp.async.bulk.tensor 2-D load into a 3-stage mbarrier ring, 2 tiles
+// ahead, and TMA's out-of-bounds zero fill IS the zero padding on all four
+// sides.  The box starts 4 columns (16 bytes) left of the tile because the
+// innermost start coordinate must be a multiple of 16 bytes -- measured on
+// the box with scripts/micro/tma_probe.cu: x = -2 or 250 (floats) faults with
+// an illegal instruction, x = -4 / 252 and any row coordinate work, out-of-
+// range parts zero-filled.  Each thread computes a 2 x 4 patch
+// (two x-adjacent outputs, four rows) with the paired FP32 instruction FFMA2
+// -- the two outputs share every filter weight -- and slides down its
+// (2 + 2r)-wide window with 8-byte shared loads, 8 output rows per thread so
+// every loaded row feeds up to 2r + 1 of them; outputs leave as 8-byte
+// streaming stores.  Other shapes use the simple kernel below.
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace jacc_k {
 namespace {
 
 constexpr int TX = 32, TY = 32, Q = 4;     // tile, outputs per thread (rows)
+
+constexpr int PX = 64, PY = 64, kStages = 3;   // TMA path: output tile, ring depth
+constexpr int QR = 8;                          // TMA path: output rows per thread (x 2 columns)
+template <int R>
+struct Box {
+    static constexpr int X0 = 4;                      // box starts 4 floats (16 B) left of the tile
+    static constexpr int W = PX + 2 * X0;             // 72: covers x0 - 4 .. x0 + 67
+    static constexpr int H = PY + 2 * R;
+    static constexpr int kBytes = W * H * 4;
+    static constexpr int kStride = (kBytes + 1023) & ~1023;   // TMA destinations: 128-byte (here 1 KiB) aligned
+    static constexpr int kSmem = kStages * kStride + 1024;    // + alignment slack of the dynamic base
+    static_assert(R <= X0 && ((X0 - R) & 1) == 0, "window start must be even (8-byte shared loads)");
+};
+
+__device__ __forceinline__ void st_stream2(float *p, float2 v) {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t H,
+                                                            int64_t W, const float *__restrict__ filt,
+                                                            float *__restrict__ out, int tiles_x, int ntiles) {
+    constexpr int K = 2 * R + 1, BW = Box<R>::W;
+    constexpr uint32_t kBytes = Box<R>::kBytes;
+    constexpr int kStrideF = Box<R>::kStride / 4;            // floats between ring stages
+    extern __shared__ uint8_t smem_raw[];
+    // kStages boxes, 1 KiB aligned; offset arithmetic on the shared array (not
+    // through an integer) keeps the loads below LDS instead of generic LD
+    float *ring = reinterpret_cast<float *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
+    __shared__ __align__(8) uint64_t bar[kStages];
+    const int tid = threadIdx.x, cx = tid & 31, rg = tid >> 5;   // column pair, row group (QR rows)
+    float2 ff[K * K];                                            // flipped filter, (w, w) pairs
+#pragma unroll
+    for (int m = 0; m < K; ++m)
+#pragma unroll
+        for (int n = 0; n < K; ++n) {
+            const float w = __ldg(filt + (2 * R - m) * K + (2 * R - n));
+            ff[m * K + n] = make_float2(w, w);
+        }
+    // (the map's address is taken directly in the kernel body: through a
+    // capturing lambda nvcc 12.9 passed the wrong parameter slot to UTMALDG)
+#define CONV_ISSUE(t_, stage_)                                                                     \
+    do {                                                                                           \
+        const int x0_ = ((t_) % tiles_x) * PX, y0_ = ((t_) / tiles_x) * PY;                       \
+        const uint32_t b_ = tc::smem_u32(&bar[(stage_)]);                                          \
+        tc::mbar_expect_tx(b_, kBytes);                                                            \
+        tc::tma_load_2d(tc::smem_u32(ring + (stage_) * kStrideF), &map, x0_ - Box<R>::X0, y0_ - R, b_); \
+    } while (0)
+    if (tid == 0) {
+        tc::tma_prefetch(&map);
+        for (int i = 0; i < kStages; ++i) tc::mbar_init(tc::smem_u32(&bar[i]), 1);
+        tc::fence_barrier_init();
+        for (int i = 0; i < kStages - 1; ++i)
+            if (blockIdx.x + i * (int)gridDim.x < ntiles) CONV_ISSUE(blockIdx.x + i * (int)gridDim.x, i);
+    }
+    __syncthreads();
+    // tile coordinates advanced incrementally (no division per tile)
+    const int dtx = (int)gridDim.x % tiles_x, dty = (int)gridDim.x / tiles_x;
+    int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    int k = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int stage = k % kStages;
+        const int tn = t + (kStages - 1) * gridDim.x;   // refill the stage freed in iteration k - 1
+        if (tid == 0 && tn < ntiles) CONV_ISSUE(tn, (k + kStages - 1) % kStages);
+        tc::mbar_wait(tc::smem_u32(&bar[stage]), (k / kStages) & 1);
+        const float *S = ring + stage * kStrideF + (rg * QR) * BW + 2 * cx + (Box<R>::X0 - R);
+        float2 acc[QR];
+#pragma unroll
+        for (int q = 0; q < QR; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < QR + 2 * R; ++w) {   // window row w feeds output rows q = w - m
+            float v[2 + 2 * R];
+#pragma unroll
+            for (int c = 0; c <= R; ++c) {
+                const float2 p = *reinterpret_cast<const float2 *>(S + w * BW + 2 * c);
+                v[2 * c] = p.x;
+                v[2 * c + 1] = p.y;
+            }
+#pragma unroll
+            for (int q = 0; q < QR; ++q) {
+                const int m = w - q;
+                if (m < 0 || m > 2 * R) continue;
+#pragma unroll
+                for (int n = 0; n < K; ++n) acc[q] = __ffma2_rn(ff[m * K + n], make_float2(v[n], v[n + 1]), acc[q]);
+            }
+        }
+        const int64_t xo = (int64_t)tx * PX + 2 * cx, yo = (int64_t)ty * PY + rg * QR;
+        if (xo < W) {
+#pragma unroll
+            for (int q = 0; q < QR; ++q)
+                if (yo + q < H) st_stream2(out + (yo + q) * W + xo, acc[q]);
+        }
+        tx += dtx;
+        ty += dty;
+        if (tx >= tiles_x) {
+            tx -= tiles_x;
+            ++ty;
+        }
+        __syncthreads();   // every thread is done with `stage` before it is refilled
+    }
+#undef CONV_ISSUE
+}
 
 template <int R>
 __global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ img, int64_t H, int64_t W,
@@ -60,11 +179,40 @@ __global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ i
     }
 }
 
+template <int R>
+cudaError_t launch_tma(const float *img, int64_t H, int64_t W, const float *filt, float *out, cudaStream_t st,
+                       bool *done) {
+    *done = false;
+    CUtensorMap map;
+    if (!tc::make_map_2d(&map, img, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, H, W, W * 4, Box<R>::H, Box<R>::W, 0))
+        return cudaSuccess;   // no tensor map for this shape: the simple kernel runs
+    const int smem = Box<R>::kSmem;
+    cudaError_t e = set_max_dyn_smem((const void *)conv2d_tma_kernel<R>, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles_x = (W + PX - 1) / PX, ntiles = tiles_x * ((H + PY - 1) / PY);
+    int64_t grid = (int64_t)sm_count() * blocks_per_sm((const void *)conv2d_tma_kernel<R>, 256, smem);
+    if (grid > ntiles) grid = ntiles;
+    conv2d_tma_kernel<R><<<(unsigned)grid, 256, smem, st>>>(map, H, W, filt, out, (int)tiles_x, (int)ntiles);
+    *done = true;
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,
                        cudaStream_t st, int *launches) {
     if (H <= 0 || W <= 0) return cudaSuccess;
+    // TMA path: 16-byte aligned rows, int32 tile coordinates
+    if (radius == 2 && W % 4 == 0 && aligned16(img) && (W + PX) < (1ll << 31) &&
+        (H + PY) < (1ll << 31) && ((W + PX - 1) / PX) * ((H + PY - 1) / PY) < (1ll << 31)) {
+        bool done = false;
+        cudaError_t e = launch_tma<2>(img, H, W, filt, out, st, &done);
+        if (e != cudaSuccess) return e;
+        if (done) {
+            ++*launches;
+            return cudaSuccess;
+        }
+    }
     dim3 grid((unsigned)((W + TX - 1) / TX), (unsigned)((H + TY - 1) / TY));
     switch (radius) {
         case 1: conv2d_kernel<1><<<grid, 256, 0, st>>>(img, H, W, filt, out); break;

@@ -100,7 +100,9 @@ inline encode_fn_t get_encode() {
 }
 
 // 2-D map over a row-major [rows x cols] matrix of `esize`-byte elements
-// (row stride `ld_bytes`), box [box_rows x box_cols], swizzle `sw` bytes.
+// (row stride `ld_bytes`), box [box_rows x box_cols], swizzle `sw` bytes
+// (0 = none: the box lands row-major, box_cols contiguous).  Out-of-bounds
+// box elements (negative or past-the-end coordinates) are filled with zeros.
 inline bool make_map_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize, int64_t rows,
                         int64_t cols, int64_t ld_bytes, int box_rows, int box_cols, int sw) {
     encode_fn_t enc = get_encode();
@@ -111,7 +113,8 @@ inline bool make_map_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt
     cuuint32_t es[2] = {1, 1};
     (void)esize;
     return enc(m, dt, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               sw == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -97,7 +97,7 @@ def main():
                        jacc.jacc_conv2d_params_t(n, n, 2, 0))
             units, kind = 8 * n * n, "GB/s"
         elif op == "corr":
-            A = synth.corr_bitsets()
+            A = synth.corr_bitsets(a.n) if a.n else synth.corr_bitsets()
             C = np.zeros((A.shape[0], A.shape[0]), np.int32)
             g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(D(A.view(np.int32)), R), g.a(D(A.view(np.int32) + 0), R),
                                                   g.a(D(C), W)],
@@ -105,7 +105,7 @@ def main():
             n = A.shape[0]
             units, kind = n * n * A.shape[1] * 32 * 2, "TFLOP/s"   # bit-ops: AND + count per bit pair
         elif op == "spmv":
-            rp, col, val = synth.banded_csr()
+            rp, col, val = synth.banded_csr(a.n, 23 * a.n) if a.n else synth.banded_csr()
             n = rp.size - 1
             x = synth.uniform_f32(n, 5, -1, 1)
             g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(D(rp), R), g.a(D(col), R), g.a(D(val), R), g.a(D(x), R),

@@ -27,8 +27,11 @@ def _conv(img, f):
     return out
 
 
+# TMA path: W % 4 == 0 and r <= 2 (ragged 64 x 32 tiles, tiny images, many
+# tiles per persistent block); the others take the simple kernel
 @pytest.mark.parametrize("H,Wd,r", [(1, 1, 2), (7, 9, 2), (33, 65, 1), (256, 256, 2), (100, 37, 3),
-                                    (64, 64, 4), (2048, 2048, 2)])
+                                    (64, 64, 4), (2048, 2048, 2), (1, 4, 2), (3, 8, 1), (97, 132, 2),
+                                    (33, 68, 1), (31, 260, 2), (1000, 1028, 2)])
 def test_conv2d_tolerance(H, Wd, r):
     img = synth.uniform_f32(H * Wd, 100 + H, -1, 1).reshape(H, Wd)
     f = synth.uniform_f32((2 * r + 1) ** 2, 200 + r, -1, 1).reshape(2 * r + 1, 2 * r + 1)
@@ -67,10 +70,12 @@ def test_spmv_tolerance(n, nnz, bw):
     assert np.all(np.abs(y - ref) <= 1e-5 * ab + 1e-30)
 
 
-def test_conv2d_delta_exact():
+@pytest.mark.parametrize("shape", [(40, 50), (40, 132)])   # simple kernel / TMA path (zero-filled halo)
+def test_conv2d_delta_exact(shape):
     f = synth.uniform_f32(25, 3).reshape(5, 5)
-    img = np.zeros((40, 50), np.float32)
-    img[0, 0] = 1.0; img[20, 30] = 1.0; img[39, 49] = 1.0
+    img = np.zeros(shape, np.float32)
+    h, w = shape
+    img[0, 0] = 1.0; img[20, 30] = 1.0; img[h - 1, w - 1] = 1.0; img[0, w - 1] = 1.0; img[h - 1, w // 2 - 5] = 1.0   # impulses >= 5 apart: responses never overlap
     out = _conv(img, f)
     ref, _ = oracle.conv2d(img, f)
     assert np.array_equal(out.astype(np.float64), ref)
