@@ -393,6 +393,78 @@ def roofline_points(torch, J, peaks, reps=10):
     return out
 
 
+def next_rows(torch, J, peaks, reps=10):
+    """SURVEY §8(f) NEXT rows, each at the paper's size and, for
+    the HBM-bound ones, at a size that is not L2-resident (the roofline
+    point); device time per launch from the task's CUDA events, L2 flushed
+    before every launch.  Units: conv2d 8 B/pixel, SpMV 8 B/non-zero + 12 B/
+    row, corr 2 ops per u8 multiply-accumulate (roof: i8 dense = 2 x bf16)."""
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph
+    R, W = J.JACC_READ, J.JACC_WRITE
+    dev = torch.device("cuda", torch.cuda.current_device())
+    flush = torch.empty(64 << 20, device=dev)
+    out = {}
+
+    def timed(build):
+        g, _ = make_graph(dev.index, n_streams=1)
+        keep = build(g)
+        ms = []
+        for i in range(reps + 2):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            g.run()
+            if i >= 2:
+                ms.append(g.task_ms(0))
+        g.destroy()
+        del keep
+        return statistics.mean(ms)
+
+    def D(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    def conv(n):
+        img = torch.rand((n, n), device=dev) * 2 - 1
+        f = D(synth.uniform_f32(25, 12, -1, 1).reshape(5, 5))
+        o = torch.empty_like(img)
+        return timed(lambda g: (g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(o, W)],
+                                           jacc.jacc_conv2d_params_t(n, n, 2, 0)), img, f, o))
+
+    def spmv(n, nnz):
+        rp, col, val = synth.banded_csr(n, nnz)
+        t = [D(rp), D(col), D(val), torch.rand(n, device=dev), torch.empty(n, device=dev)]
+        ms = timed(lambda g: (g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(t[0], R), g.a(t[1], R), g.a(t[2], R),
+                                                                  g.a(t[3], R), g.a(t[4], W)],
+                                         jacc.jacc_spmv_params_t(n, n)), t))
+        return ms, 8 * col.size + 12 * n + 4
+
+    hbm = peaks["hbm_gbs"]
+    for name, n in (("conv2d_2048", 2048), ("conv2d_16384", 16384)):
+        ms = conv(n)
+        ach = 8 * n * n / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "achieved": ach, "unit": "GB/s", "peak": hbm, "frac": ach / hbm,
+                     "note": "L2-resident (32 MB)" if n == 2048 else "roofline point (2 GiB moved)"}
+    for name, (n, nnz) in (("spmv_44609", (synth.SPMV_N, synth.SPMV_NNZ)), ("spmv_2m", (1 << 21, 23 << 21))):
+        ms, nbytes = spmv(n, nnz)
+        ach = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "achieved": ach, "unit": "GB/s", "peak": hbm, "frac": ach / hbm,
+                     "note": "L2-resident (12 MB)" if n == synth.SPMV_N else "roofline point (~0.4 GB moved)"}
+    bits = synth.corr_bitsets()
+    ta, words = bits.shape
+    A = D(bits.view(np.int32))
+    Cm = torch.empty((ta, ta), dtype=torch.int32, device=dev)
+    ms = timed(lambda g: (g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(A, R), g.a(A, R), g.a(Cm, W)],
+                                     jacc.jacc_corr_params_t(ta, ta, words)), A, Cm))
+    ops = 2 * ta * ta * words * 32
+    i8_peak = peaks["bf16_tflops"] * 2
+    out["corr_1024x16384"] = {"ms": ms, "achieved": ops / (ms * 1e-3) / 1e12, "unit": "TOPS (u8 MAC = 2)",
+                              "peak": i8_peak, "frac": ops / (ms * 1e-3) / 1e12 / i8_peak,
+                              "note": "incl. the two bit-unpack kernels; i8 peak = bf16 x 2 (nominal ratio)"}
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def _median_run_us(g, reps):
     ts = []
     for _ in range(reps):
@@ -634,6 +706,10 @@ def run_jacc(args):
             line["roofline_points_2p28"] = roofline_points(torch, J, peaks)
         except Exception as exc:   # an auxiliary measurement must not lose the bench line
             line["cfg1_task_graph"] = {"error": str(exc)[:300]}
+        try:
+            line["next_rows"] = next_rows(torch, J, peaks)
+        except Exception as exc:
+            line["next_rows"] = {"error": str(exc)[:300]}
     if not args.no_cpu_baseline and world == 1:
         total, desc, cores, parts = cpu_oracle_sample()
         line["cpu_baseline"] = {"value": 1.0 / total, "unit": UNIT, "cores": cores, "kind": "oracle",
