@@ -9,10 +9,17 @@
 // tensor cores (tcgen05 has no 1-bit kind; the legacy mma.sync b1 path lowers
 // to 8 IMMA.U8 per instruction), so:
 //   1. unpack: bitsets -> 0/1 uint8 rows (K-major), zero padded to the tile grid;
+//      (when A and B are the same bitsets -- the paper's term-by-term matrix --
+//      they are unpacked once);
 //   2. GEMM: tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32, exact),
-//      128 x 64 output tile per CTA, 128-byte K blocks staged by TMA (128B
-//      swizzle) through a 4-stage mbarrier ring, accumulator in TMEM (64
-//      columns), epilogue tcgen05.ld -> int32 stores.
+//      128 x 256 output tile per CTA (48 KB of operands per 128-byte K block
+//      for 4M multiply-adds: a 128 x 64 tile needed twice the bytes per MAC
+//      and was bound by the SM's operand feed), K blocks staged by TMA (128B
+//      swizzle) through a 4-stage mbarrier ring, accumulator in TMEM (256
+//      columns), epilogue tcgen05.ld -> int32 stores;
+//   3. split-K when the output has fewer tiles than SMs (1024 x 1024 = 32
+//      tiles): each split writes a partial tile, a small kernel adds the
+//      splits in order (integers: exact, independent of the split).
 // One warp issues TMA, one thread issues the MMAs, four warps drain TMEM.
 #include "common.cuh"
 #include "kernels.h"
@@ -21,36 +28,51 @@
 namespace jacc_k {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 128;     // BK bytes = one 128 B swizzle row of u8
+constexpr int BM = 128, BN = 256, BK = 128;    // BK bytes = one 128 B swizzle row of u8
 constexpr int kStages = 4;
 constexpr int kABytes = BM * BK, kBBytes = BN * BK;
-constexpr int kStageBytes = kABytes + kBBytes;  // 24 KB
+constexpr int kStageBytes = kABytes + kBBytes;  // 48 KB
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 64;
+constexpr int kTmemCols = BN;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
-// kind::i8: D = s32 (c_format 2), A/B unsigned 8-bit (format 0), K-major, M = 128, N = 64
+// kind::i8: D = s32 (c_format 2), A/B unsigned 8-bit (format 0), K-major, M = 128, N = 256
 constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// bitsets [t x words] -> u8 [tp x kp]: byte d of row i = bit d%32 of word d/32
+// bitsets [t x words] -> u8 [tp x kp]: byte d of row i = bit d%32 of word d/32.
+// A warp expands 16 words into one contiguous 512-byte run per store: lane l
+// writes bytes [16 l, 16 l + 16), the expansion of half (l & 1) of word l / 2
+// -- every store instruction is fully coalesced.
+__device__ __forceinline__ uint32_t expand4(uint32_t nib) {   // 4 bits -> 4 bytes (little endian)
+    return (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 | ((nib >> 3) & 1u) << 24;
+}
+
 __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t *__restrict__ bits, int64_t t, int64_t words,
                                                      uint8_t *__restrict__ x, int64_t tp, int64_t kp) {
-    const int64_t wpr = kp / 32;   // 32 bytes (one word) per thread
-    const int64_t total = tp * wpr;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = q / wpr, w = q - r * wpr;
-        const uint32_t v = (r < t && w < words) ? __ldg(bits + r * words + w) : 0u;
-        uint4 o[2];
-        uint32_t *ob = (uint32_t *)o;
+    constexpr int U = 4;   // runs per warp per pass: their loads are issued together
+    const int lane = threadIdx.x & 31;
+    const int64_t rpr = (kp + 511) / 512;    // kp is a multiple of 128: a row's last run may be partial
+    const int64_t total = tp * rpr;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q0 = warp0; q0 < total; q0 += U * nwarps) {
+        uint32_t v[U];
+        int64_t dst[U];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {   // 4 bits -> 4 bytes (little endian)
-            const uint32_t nib = (v >> (4 * b)) & 0xFu;
-            ob[b] = (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 | ((nib >> 3) & 1u) << 24;
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = q0 + u * nwarps;
+            const int64_t r = q / rpr, byte = (q - r * rpr) * 512 + 16 * lane, w = byte / 32;
+            const bool ok = q < total && byte < kp;
+            dst[u] = ok ? r * kp + byte : -1;
+            v[u] = (ok && r < t && w < words) ? __ldg(bits + r * words + w) : 0u;
         }
-        uint4 *dst = (uint4 *)(x + r * kp + w * 32);
-        dst[0] = o[0];
-        dst[1] = o[1];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (dst[u] < 0) continue;
+            const uint32_t h = (lane & 1) ? v[u] >> 16 : v[u];
+            *(uint4 *)(x + dst[u]) = make_uint4(expand4(h), expand4(h >> 4), expand4(h >> 8), expand4(h >> 12));
+        }
     }
 }
 
@@ -62,9 +84,13 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
         "l"(da), "l"(db), "r"(kIdesc), "r"(accum));
 }
 
+// C tile (m_blk, n_blk) over K blocks [kb0, kb1).  ldc = tb and bounds
+// checks when writing C directly; a padded [tap x tbp] partial (split
+// blockIdx.z) otherwise.
 __global__ void __launch_bounds__(kThreads, 1)
     corr_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   int32_t *__restrict__ C, int64_t ta, int64_t tb, int num_kb) {
+                   int32_t *__restrict__ C, int64_t ta, int64_t tb, int num_kb, int32_t *__restrict__ part,
+                   int64_t tap, int64_t tbp) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + kStages * kStageBytes);
@@ -73,6 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    tfull = tc::smem_u32(bars + 2 * kStages);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m_blk = blockIdx.y, n_blk = blockIdx.x;
+    const int per = (num_kb + gridDim.z - 1) / gridDim.z;
+    const int kb0 = blockIdx.z * per, kb1 = min(num_kb, kb0 + per);
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&map_a);
         tc::tma_prefetch(&map_b);
@@ -90,9 +118,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_d = *tmem_slot;
     if (warp == 0) {
         if (lane == 0) {   // TMA producer
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % kStages;
-                tc::mbar_wait(empty0 + 8 * s, ((kb / kStages) & 1) ^ 1);
+            for (int i = 0; i < kb1 - kb0; ++i) {
+                const int s = i % kStages, kb = kb0 + i;
+                tc::mbar_wait(empty0 + 8 * s, ((i / kStages) & 1) ^ 1);
                 uint8_t *st = smem + s * kStageBytes;
                 tc::mbar_expect_tx(full0 + 8 * s, kStageBytes);
                 tc::tma_load_2d(tc::smem_u32(st), &map_a, kb * BK, m_blk * BM, full0 + 8 * s);
@@ -101,15 +129,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {   // MMA issuer
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % kStages;
-                tc::mbar_wait(full0 + 8 * s, (kb / kStages) & 1);
+            for (int i = 0; i < kb1 - kb0; ++i) {
+                const int s = i % kStages;
+                tc::mbar_wait(full0 + 8 * s, (i / kStages) & 1);
                 tc::fence_after();
                 const uint32_t a = tc::smem_u32(smem + s * kStageBytes), b = a + kABytes;
 #pragma unroll
                 for (int k = 0; k < BK / 32; ++k)   // K = 32 bytes per MMA
                     mma_i8(tmem_d, tc::desc_kmajor(a + 32 * k, 128), tc::desc_kmajor(b + 32 * k, 128),
-                           (kb | k) != 0);
+                           (i | k) != 0);
                 tc::commit(empty0 + 8 * s);
             }
             tc::commit(tfull);
@@ -119,13 +147,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait(tfull, 0);
         tc::fence_after();
         const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
-#pragma unroll
+        int32_t *prow = part ? part + ((int64_t)blockIdx.z * tap + row) * tbp : nullptr;
+#pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
             JACC_TMEM_LD_32(tmem_d + ((uint32_t)(q * 32) << 16) + c * 32, r);
             tc::wait_ld();
-            if (row < ta) {
-                const int64_t col0 = (int64_t)n_blk * BN + c * 32;
+            const int64_t col0 = (int64_t)n_blk * BN + c * 32;
+            if (prow) {   // padded partial tile: 16-byte stores, no bounds
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *(int4 *)(prow + col0 + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
+            } else if (row < ta) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     if (col0 + j < tb) C[row * tb + col0 + j] = (int32_t)r[j];
@@ -140,11 +173,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// C[i][j] = sum over splits of the partial tiles, in split order (exact).
+// One row per blockIdx.y; 16-byte loads of the padded partials.
+__global__ void __launch_bounds__(256) split_sum_kernel(const int32_t *__restrict__ part, int splits, int64_t tap,
+                                                        int64_t tbp, int32_t *__restrict__ C, int64_t ta,
+                                                        int64_t tb) {
+    const int64_t i = blockIdx.y;
+    const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (j0 >= tb) return;
+    int4 acc = make_int4(0, 0, 0, 0);
+    for (int s = 0; s < splits; ++s) {
+        const int4 v = __ldg((const int4 *)(part + ((int64_t)s * tap + i) * tbp + j0));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    int32_t *c = C + i * tb + j0;
+    if (j0 + 4 <= tb && (((uintptr_t)c) & 15) == 0) {
+        *(int4 *)c = acc;
+    } else {
+        const int32_t a[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int k = 0; k < 4 && j0 + k < tb; ++k) c[k] = a[k];
+    }
+}
+
+// K splits: enough CTAs to cover the SMs, each split >= 8 K blocks.
+int corr_splits(int64_t ta, int64_t tb, int64_t words) {
+    const int64_t tiles = (round_up(ta, BM) / BM) * (round_up(tb, BN) / BN);
+    const int64_t num_kb = round_up(words * 32 > 0 ? words * 32 : 1, BK) / BK;
+    int64_t s = sm_count() / (tiles > 0 ? tiles : 1);
+    if (s > num_kb / 8) s = num_kb / 8;
+    return (int)(s < 1 ? 1 : s > 16 ? 16 : s);
+}
+
 }  // namespace
 
 size_t corr_ws_bytes(int64_t ta, int64_t tb, int64_t words) {
     const int64_t kp = round_up(words * 32 > 0 ? words * 32 : 1, BK);
-    return (size_t)(round_up(ta > 0 ? ta : 1, BM) + round_up(tb > 0 ? tb : 1, BN)) * kp + 2048;
+    const int64_t tap = round_up(ta > 0 ? ta : 1, BM), tbp = round_up(tb > 0 ? tb : 1, BN);
+    const int splits = corr_splits(ta, tb, words);
+    return (size_t)(tap + tbp) * kp + 2048 + (splits > 1 ? (size_t)splits * tap * tbp * 4 + 1024 : 0);
 }
 
 cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int64_t tb, int64_t words, int32_t *C,
@@ -155,18 +221,33 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
     uint8_t *xa = (uint8_t *)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
     uint8_t *xb = xa + tap * kp;
     const int grid_u = sm_count() * 8;
-    unpack_kernel<<<grid_u, 256, 0, st>>>(A, ta, words, xa, tap, kp);
-    unpack_kernel<<<grid_u, 256, 0, st>>>(B, tb, words, xb, tbp, kp);
-    *launches += 2;
+    const bool same = A == B && ta == tb;   // C = X X^T: one unpacked copy serves both operands
+    unpack_kernel<<<grid_u, 256, 0, st>>>(A, ta, words, xa, same ? tbp : tap, kp);
+    ++*launches;
+    if (same) {
+        xb = xa;
+    } else {
+        unpack_kernel<<<grid_u, 256, 0, st>>>(B, tb, words, xb, tbp, kp);
+        ++*launches;
+    }
     CUtensorMap ma, mb;
     if (!tc::make_map_2d(&ma, xa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tap, kp, kp, BM, BK, 128) ||
         !tc::make_map_2d(&mb, xb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tbp, kp, kp, BN, BK, 128))
         return cudaErrorInvalidValue;
     cudaError_t e = set_max_dyn_smem((const void *)corr_i8_kernel, kSmemBytes);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)(tbp / BN), (unsigned)(tap / BM));
-    corr_i8_kernel<<<grid, kThreads, kSmemBytes, st>>>(ma, mb, C, ta, tb, (int)(kp / BK));
+    const int splits = corr_splits(ta, tb, words);
+    int32_t *part = nullptr;
+    if (splits > 1)
+        part = (int32_t *)(((uintptr_t)(xb + tbp * kp) + 1023) & ~(uintptr_t)1023);
+    dim3 grid((unsigned)(tbp / BN), (unsigned)(tap / BM), (unsigned)splits);
+    corr_i8_kernel<<<grid, kThreads, kSmemBytes, st>>>(ma, mb, C, ta, tb, (int)(kp / BK), part, tap, tbp);
     ++*launches;
+    if (part) {
+        split_sum_kernel<<<dim3((unsigned)((tb + 1023) / 1024), (unsigned)ta), 256, 0, st>>>(part, splits, tap, tbp,
+                                                                                            C, ta, tb);
+        ++*launches;
+    }
     return cudaGetLastError();
 }
 
