@@ -363,7 +363,10 @@ int jacc_graph_dump(jacc_graph_t *g, char *buf, size_t cap, size_t *needed);
  * copies it in again (reading R5).  Errors: _NOT_FOUND, _STATE.          */
 int jacc_buffer_invalidate(jacc_graph_t *g, const void *host_ptr);
 
-/* Implicit sync, then release the device copies, events and owned streams. */
+/* Implicit sync, then release the device copies, events and owned streams.
+ * A connected JACC_GRAPH_P2P graph first waits (on the device) until every
+ * rank has reached its destroy, so no peer stores into a freed window:
+ * every rank must destroy its graph (SPMD).                              */
 int jacc_graph_destroy(jacc_graph_t *g);
 
 /* ---- peer windows (JACC_GRAPH_P2P, reading R23) -------------------------

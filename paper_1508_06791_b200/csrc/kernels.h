@@ -81,6 +81,10 @@ size_t peer_allreduce_stage_bytes(int64_t n, int esz, int world);
 cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, cudaStream_t st, int *launches);
 cudaError_t peer_allgather(const PeerOp &op, const void *send, int64_t bytes, cudaStream_t st, int *launches);
 cudaError_t peer_broadcast(const PeerOp &op, int root, int64_t bytes, cudaStream_t st, int *launches);
+// every rank: returns (on the stream) once all ranks reached it -- used before
+// a window is unmapped and freed (a peer may still owe it a flag store)
+cudaError_t peer_barrier(const PeerCtx &c, int slot, cudaStream_t st);
+constexpr int kPeerBarrierSlot = kPeerSlots - 1;   // reserved: collective tasks use 0 .. kPeerSlots - 2
 
 // 2D convolution
 cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,

@@ -87,6 +87,15 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(PeerCtx c, int slot, con
     else if (threadIdx.x == 0 && c.rank != root) peer::wait_ge(peer::flag(c.self, peer::kDataOff, slot, root), e);
 }
 
+// All ranks: every earlier kernel of this rank's stream has finished (stream
+// order) and so have every peer's (each waits for all ranks' flags): after
+// this kernel no peer will store into this rank's window again.
+__global__ void barrier_kernel(PeerCtx c, int slot) {
+    const uint64_t e = peer::epoch(c, slot);
+    if (threadIdx.x == 0) peer::publish_data(c, slot, e);
+    peer::wait_all_data(c, slot, e);
+}
+
 int copy_grid(int64_t bytes) {
     // ~64 KiB per block, at most 32 blocks (a few SMs: the copy is NVLink-bound)
     int64_t g = (bytes + (64 << 10) - 1) / (64 << 10);
@@ -132,4 +141,11 @@ cudaError_t peer_broadcast(const PeerOp &op, int root, int64_t bytes, cudaStream
     return cudaGetLastError();
 }
 
+}  // namespace jacc_k
+
+namespace jacc_k {
+cudaError_t peer_barrier(const PeerCtx &c, int slot, cudaStream_t st) {
+    barrier_kernel<<<1, 32, 0, st>>>(c, slot);
+    return cudaGetLastError();
+}
 }  // namespace jacc_k

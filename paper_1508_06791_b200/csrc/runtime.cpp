@@ -676,8 +676,9 @@ int prepare_peer(jacc_graph *g) {
     if (g->cfg.world > 1 && !g->peer_connected) return fail(JACC_ERR_STATE, "P2P graph not connected");
     for (Task &T : g->tasks) {
         if (!is_collective(T.op)) continue;
-        if (T.slot >= jacc_k::kPeerSlots)
-            return fail(JACC_ERR_UNSUPPORTED, "P2P graph with more than %d collective tasks", jacc_k::kPeerSlots);
+        if (T.slot >= jacc_k::kPeerBarrierSlot)
+            return fail(JACC_ERR_UNSUPPORTED, "P2P graph with more than %d collective tasks",
+                        jacc_k::kPeerBarrierSlot);
         const TaskArg &a = T.args[0];
         if (T.op == JACC_OP_ALLREDUCE_SUM) {
             if (T.peer_off < 0) {
@@ -1427,6 +1428,12 @@ int jacc_graph_destroy(jacc_graph_t *g) {
     if (g->res_ready) {
         cudaSetDevice(g->cfg.device);
         sync_all(g);
+        // JACC_GRAPH_P2P: wait until every rank has reached destroy before this
+        // window is freed -- a slower peer may still owe it a flag store
+        // (e.g. a broadcast's "ready" that no rank waits for)
+        if (g->peer_connected && g->cfg.world > 1 && g->state != ST_FAILED &&
+            jacc_k::peer_barrier(peer_ctx(g), jacc_k::kPeerBarrierSlot, g->compute[0]) == cudaSuccess)
+            cudaStreamSynchronize(g->compute[0]);
         for (Buffer &B : g->bufs) {
             if (!B.device && !B.in_window) dev_free(g, B.dptr, B.bytes);
             if (B.ev_h2d) cudaEventDestroy(B.ev_h2d);
