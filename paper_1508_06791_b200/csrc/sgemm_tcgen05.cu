@@ -155,11 +155,17 @@ __global__ void __launch_bounds__(256) split_bt_kernel(const float *__restrict__
 constexpr int kChunkKB = 256 / BK;
 constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quarter, 128 columns each
 
+// Split-K (blockIdx.y = split, gridDim.y > 1 only when the output has fewer
+// tiles than SMs): a split covers whole 256-wide K chunks and writes its
+// partial tile to part[split][Mp][Np]; a second kernel adds the splits in
+// order.  Every element's sum is then ((chunks of split 0) + (chunks of
+// split 1)) + ... -- fixed for a given shape, but not the unsplit order, so
+// row blocks are bitwise-equal across shardings only when neither splits.
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                        float *__restrict__ C, int64_t M, int64_t N, int64_t ldc, int num_kb, int num_m,
-                       int num_n) {
+                       int num_n, float *__restrict__ part, int64_t Mp, int64_t Np) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + kStages * kStageBytes);
@@ -177,7 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gm = min(num_m - first_m, kGroupM);
     const int m_blk = first_m + (pid % per_group) % gm;
     const int n_blk = (pid % per_group) / gm;
-    const int nchunks = (num_kb + kChunkKB - 1) / kChunkKB;
+    const int all_chunks = (num_kb + kChunkKB - 1) / kChunkKB;
+    const int per_split = (all_chunks + gridDim.y - 1) / gridDim.y;
+    const int c_begin = blockIdx.y * per_split, c_end = min(all_chunks, c_begin + per_split);
+    const int kb_begin = c_begin * kChunkKB, kb_end = min(num_kb, c_end * kChunkKB);
+    const int nchunks = c_end > c_begin ? c_end - c_begin : 0;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&map_ahi); tma_prefetch(&map_alo); tma_prefetch(&map_bhi); tma_prefetch(&map_blo);
@@ -201,9 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {   // ---- TMA producer
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
+            for (int kb = kb_begin; kb < kb_end; ++kb) {
+                const int i = kb - kb_begin;
+                const int s = i % kStages;
+                const uint32_t ph = (i / kStages) & 1;
                 mbar_wait(empty_bar0 + 8 * s, ph ^ 1);
                 uint8_t *st = smem + s * kStageBytes;
                 const uint32_t fb = full_bar0 + 8 * s;
@@ -216,12 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {   // ---- MMA issuer (one thread for the whole CTA)
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
-                const int chunk = kb / kChunkKB, buf = chunk & 1;
-                const bool first = (kb % kChunkKB) == 0;
-                const bool last = (kb % kChunkKB) == kChunkKB - 1 || kb == num_kb - 1;
+            for (int kb = kb_begin; kb < kb_end; ++kb) {
+                const int i = kb - kb_begin;   // split-local: chunk = i / kChunkKB (splits start on chunks)
+                const int s = i % kStages;
+                const uint32_t ph = (i / kStages) & 1;
+                const int chunk = i / kChunkKB, buf = chunk & 1;
+                const bool first = (i % kChunkKB) == 0;
+                const bool last = (i % kChunkKB) == kChunkKB - 1 || kb == kb_end - 1;
                 const uint32_t tmem_d = tmem_base + buf * BN;
                 if (first) {   // the epilogue has drained this buffer's previous chunk
                     mbar_wait(tempty0 + 8 * buf, ((chunk >> 1) & 1) ^ 1);
@@ -266,7 +278,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) tc::mbar_arrive(tempty0 + 8 * buf);
         }
         const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
-        if (row < M) {
+        if (part) {   // split partial: padded [Mp x Np], 16-byte stores, no bounds
+            float *prow = part + ((int64_t)blockIdx.y * Mp + row) * Np + (int64_t)n_blk * BN + h * 128;
+#pragma unroll
+            for (int j = 0; j < 128; j += 4)
+                *(float4 *)(prow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else if (row < M) {
             float *crow = C + row * ldc;
             const int64_t col0 = (int64_t)n_blk * BN + h * 128;
             if (col0 + 128 <= N && ((ldc & 3) == 0) && (((uintptr_t)C & 15) == 0)) {
@@ -288,6 +305,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// C = sum of the split partials, in split order.  One row per blockIdx.y,
+// four columns per thread (16-byte partial loads; Np is a multiple of 256).
+__global__ void __launch_bounds__(256) split_sum_f32_kernel(const float *__restrict__ part, int splits, int64_t Mp,
+                                                            int64_t Np, float *__restrict__ C, int64_t M, int64_t N,
+                                                            int64_t ldc) {
+    const int64_t i = blockIdx.y;
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= M || j >= N) return;
+    float4 acc = __ldg((const float4 *)(part + i * Np + j));
+    for (int s = 1; s < splits; ++s) {
+        const float4 v = __ldg((const float4 *)(part + ((int64_t)s * Mp + i) * Np + j));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float *c = C + i * ldc + j;
+    if (j + 4 <= N && (((uintptr_t)c) & 15) == 0) {
+        *(float4 *)c = acc;
+    } else {
+        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int k = 0; k < 4 && j + k < N; ++k) c[k] = a[k];
+    }
+}
+
+// K splits for a grid of `tiles` output tiles: only when the tiles leave SMs
+// idle; whole 256-wide chunks per split.
+int sgemm_splits(int64_t tiles, int64_t Kp) {
+    const int64_t chunks = (Kp / BK + kChunkKB - 1) / kChunkKB;
+    const int sms = sm_count();
+    if (tiles >= sms || chunks < 2) return 1;
+    int64_t s = sms / tiles;
+    if (s > chunks) s = chunks;
+    if (s > 8) s = 8;
+    // equal chunk counts per split (no empty trailing split)
+    while (s > 1 && (chunks + s - 1) / s * (s - 1) >= chunks) --s;
+    return (int)(s < 1 ? 1 : s);
+}
+
 // ------------------------------------------------------------ host side
 bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int box_rows) {
     return tc::make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, kp, kp * 4, box_rows, BK, kSw);
@@ -298,7 +351,8 @@ bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int b
 size_t sgemm_3xtf32_ws_bytes(const jacc_sgemm_params_t *p) {
     const int64_t Mp = round_up(p->M > 0 ? p->M : 1, BM), Np = round_up(p->N > 0 ? p->N : 1, BN),
                   Kp = round_up(p->K > 0 ? p->K : 1, BK);
-    return (size_t)(2 * Mp * Kp + 2 * Np * Kp) * 4 + 4096;
+    const int splits = sgemm_splits((Mp / BM) * (Np / BN), Kp);
+    return (size_t)(2 * Mp * Kp + 2 * Np * Kp) * 4 + 4096 + (splits > 1 ? (size_t)splits * Mp * Np * 4 + 1024 : 0);
 }
 
 cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sgemm_params_t *p, void *ws,
@@ -326,9 +380,16 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
     cudaError_t e = set_max_dyn_smem((const void *)gemm_3xtf32_kernel, kSmemBytes);
     if (e != cudaSuccess) return e;
     const int num_m = (int)(Mp / BM), num_n = (int)(Np / BN);
-    gemm_3xtf32_kernel<<<num_m * num_n, kThreads, kSmemBytes, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc,
-                                                           (int)(Kp / BK), num_m, num_n);
+    const int splits = sgemm_splits((int64_t)num_m * num_n, Kp);
+    float *part = splits > 1 ? (float *)(((uintptr_t)(blo + Np * Kp) + 1023) & ~(uintptr_t)1023) : nullptr;
+    gemm_3xtf32_kernel<<<dim3(num_m * num_n, splits), kThreads, kSmemBytes, st>>>(
+        m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc, (int)(Kp / BK), num_m, num_n, part, Mp, Np);
     ++*launches;
+    if (part) {
+        split_sum_f32_kernel<<<dim3((unsigned)((N + 1023) / 1024), (unsigned)M), 256, 0, st>>>(part, splits, Mp, Np,
+                                                                                             C, M, N, p->ldc);
+        ++*launches;
+    }
     return cudaGetLastError();
 }
 
