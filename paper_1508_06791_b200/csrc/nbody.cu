@@ -160,26 +160,13 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_kernel(const float
     }
 }
 
-// Double-buffered variant of the kernel above: two tile buffers, the next
-// tile's raw float4s arriving by cp.async into `stage` while the current tile
-// is summed, one barrier per tile.  Measured (ms per step at 2^17 bodies,
-// target shards 1/2/4/8): single 6.103 / 3.382 / 1.724 / 0.836, double
-// 6.201 / 3.104 / 1.651 / 0.846 -- double buffering pays when the grid is
-// only a few waves deep (SMs then hold few blocks and a tile load's L2
-// latency is not covered by the others); its per-tile overhead costs 1.5 %
-// when many waves keep every SM full.  (Kept as a separate kernel: a merged
-// template with both loops compiled 2 % slower in both modes.)
-template <int P, int MINB, int UNR>
-__global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
-                                                               int64_t n_tgt, int64_t tgt_offset, float eps2,
-                                                               float4 *__restrict__ part) {
-    constexpr int T = 2 * P;
-    // double-buffered tiles, per source (x, x, y, y), (z, z, m, m); the next
-    // tile's raw float4s land in `stage` by cp.async while this one is summed
-    __shared__ float4 tile[2][2 * kTile];
-    __shared__ float4 stage[kTile];
-    const int64_t t0 = (int64_t)blockIdx.x * (kBlock * T);
-    const int64_t j_begin = (int64_t)blockIdx.y * kChunk;
+// One work unit of the double-buffered kernel: kBlock * 2P targets starting at
+// t0, sources of chunk `chunk`; tile / stage are the block's shared buffers.
+template <int P, int UNR>
+__device__ __forceinline__ void partial_unit_db(const float4 *__restrict__ pos_src, int64_t n_src, int64_t n_tgt,
+                                                int64_t tgt_offset, float eps2, float4 *__restrict__ part, int64_t t0,
+                                                int64_t chunk, float4 (*tile)[2 * kTile], float4 *stage) {
+    const int64_t j_begin = chunk * kChunk;
     const int64_t j_end = min(j_begin + kChunk, n_src);
     float2 nx[P], ny[P], nz[P], ax[P], ay[P], az[P];    // nx = -x of the target pair
     auto load_t = [&](int k) {
@@ -220,6 +207,7 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const fl
         }
         return same;
     };
+    __syncthreads();   // the previous unit of this block is done with tile / stage
     fetch(j_begin);
     float m0 = pos_src[j_begin].w;
     bool equal_mass = __syncthreads_and(expand(0, m0));
@@ -258,12 +246,58 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const fl
         m0 = m0n;
         buf ^= 1;
     }
-    float4 *out = part + (int64_t)blockIdx.y * n_tgt;
+    float4 *out = part + chunk * n_tgt;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         const int64_t ta = t0 + threadIdx.x + (2 * p) * kBlock, tb = ta + kBlock;
         if (ta < n_tgt) out[ta] = make_float4(ax[p].x, ay[p].x, az[p].x, 0.f);
         if (tb < n_tgt) out[tb] = make_float4(ax[p].y, ay[p].y, az[p].y, 0.f);
+    }
+}
+
+// Double-buffered variant of the kernel above: two tile buffers, the next
+// tile's raw float4s arriving by cp.async into `stage` while the current tile
+// is summed, one barrier per tile.  Measured (ms per step at 2^17 bodies,
+// target shards 1/2/4/8): single 6.103 / 3.382 / 1.724 / 0.836, double
+// 6.201 / 3.104 / 1.651 / 0.846 -- double buffering pays when the grid is
+// only a few waves deep (SMs then hold few blocks and a tile load's L2
+// latency is not covered by the others); its per-tile overhead costs 1.5 %
+// when many waves keep every SM full.  (Kept as a separate kernel: a merged
+// template with both loops compiled 2 % slower in both modes.)
+template <int P, int MINB, int UNR>
+__global__ void __launch_bounds__(kBlock, MINB) nbody_partial_db_kernel(const float4 *__restrict__ pos_src, int64_t n_src,
+                                                               int64_t n_tgt, int64_t tgt_offset, float eps2,
+                                                               float4 *__restrict__ part) {
+    __shared__ float4 tile[2][2 * kTile];
+    __shared__ float4 stage[kTile];
+    partial_unit_db<P, UNR>(pos_src, n_src, n_tgt, tgt_offset, eps2, part, (int64_t)blockIdx.x * (kBlock * 2 * P),
+                            blockIdx.y, tile, stage);
+}
+
+// Mixed grid for target shards a few waves deep: the first n_big units (in
+// dispatch order) cover targets [0, t_big) with 3 target pairs per thread --
+// the most efficient per interaction -- and fill whole waves; the remaining
+// targets follow as 1-pair units, a third of the size, so the last, partial
+// wave is made of small units instead of leaving most SMs idle behind a few
+// large ones.  1-D grid; unit u < n_big: target block u % nb_big of chunk
+// u / nb_big.  Which thread computes a target never changes the order of its
+// sum (chunk partials, tile order), so results are bitwise those of any
+// other variant.
+template <int MINB, int UNR>
+__global__ void __launch_bounds__(kBlock, MINB) nbody_partial_mixed_kernel(const float4 *__restrict__ pos_src,
+                                                                  int64_t n_src, int64_t n_tgt, int64_t tgt_offset,
+                                                                  float eps2, float4 *__restrict__ part, int nb_big,
+                                                                  int64_t n_big, int64_t t_big, int nb_small) {
+    __shared__ float4 tile[2][2 * kTile];
+    __shared__ float4 stage[kTile];
+    const int64_t u = blockIdx.x;
+    if (u < n_big) {
+        partial_unit_db<3, UNR>(pos_src, n_src, n_tgt, tgt_offset, eps2, part, (u % nb_big) * (kBlock * 6),
+                                u / nb_big, tile, stage);
+    } else {
+        const int64_t v = u - n_big;
+        partial_unit_db<1, UNR>(pos_src, n_src, n_tgt, tgt_offset, eps2, part, t_big + (v % nb_small) * (kBlock * 2),
+                                v / nb_small, tile, stage);
     }
 }
 
@@ -363,6 +397,33 @@ Variant variant(int64_t n_tgt, int64_t nchunks) {
     return fam[best];
 }
 
+// Mixed grid (nbody_partial_mixed_kernel) for grids a few waves deep: whole
+// waves of 3-pair units, the rest of the targets as 1-pair units.
+struct Mixed {
+    int nb_big, nb_small;
+    int64_t n_big, t_big;
+};
+bool mixed_plan(int64_t n_tgt, int64_t nchunks, Mixed *m) {
+    const int sms = sm_count();
+    const int occ = blocks_per_sm((const void *)nbody_partial_mixed_kernel<1, 4>, kBlock, 0);
+    const int64_t slots = (int64_t)occ * sms;
+    const int64_t big = kBlock * 6, small = kBlock * 2;
+    const int64_t big_units = (n_tgt + big - 1) / big * nchunks;
+    const int64_t full_waves = big_units / slots;
+    // up to 8 waves of 3-pair units; deeper grids already keep the SMs full
+    // (measured, ms per step at 2^17 bodies, target shard 1/2 / 1/4 / 1/8:
+    // single-variant kernels 3.054 / 1.663 / 0.848, mixed 3.118 / 1.589 / 0.817)
+    if (full_waves < 1 || big_units > 8 * slots) return false;
+    int64_t nb_big = full_waves * slots / nchunks;
+    if (nb_big * big > n_tgt) nb_big = n_tgt / big;
+    if (nb_big < 1) return false;
+    m->nb_big = (int)nb_big;
+    m->n_big = nb_big * nchunks;
+    m->t_big = nb_big * big;
+    m->nb_small = (int)((n_tgt - m->t_big + small - 1) / small);
+    return m->n_big + (int64_t)m->nb_small * nchunks < 0x7fffffff;
+}
+
 }  // namespace
 
 size_t nbody_ws_bytes(int64_t n_src, int64_t n_tgt) {
@@ -381,11 +442,17 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
         cudaError_t e = cudaMemsetAsync(part, 0, n_tgt * sizeof(float4), st);
         if (e != cudaSuccess) return e;
     } else {
-        const Variant v = variant(n_tgt, nchunks);
-        const int64_t per_block = (int64_t)kBlock * v.tpt;
         if (nchunks > 65535) return cudaErrorInvalidConfiguration;   // > 134M sources: shard further
-        dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nchunks);
-        v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);
+        Mixed mx;
+        if (mixed_plan(n_tgt, nchunks, &mx)) {
+            nbody_partial_mixed_kernel<1, 4><<<(unsigned)(mx.n_big + (int64_t)mx.nb_small * nchunks), kBlock, 0, st>>>(
+                pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part, mx.nb_big, mx.n_big, mx.t_big, mx.nb_small);
+        } else {
+            const Variant v = variant(n_tgt, nchunks);
+            const int64_t per_block = (int64_t)kBlock * v.tpt;
+            dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nchunks);
+            v.fn<<<grid, kBlock, 0, st>>>(pos_src, n_src, n_tgt, p->tgt_offset, p->eps2, part);
+        }
         ++*launches;
     }
     auto fin = pop ? nbody_finish_kernel<true> : nbody_finish_kernel<false>;

@@ -384,10 +384,11 @@ def test_nbody_unequal_masses(case):
 
 def test_nbody_full_size_mixed_masses_and_kernel_variants():
     """2^17 bodies: the full grid takes the single-buffered kernel (many
-    waves), a 1/2 and a 1/8 target shard the double-buffered one (few waves,
-    P = 3 and P = 2) -- with unequal masses (general tile path) the sampled
-    accelerations match the oracle, and every shard is bitwise equal to the
-    full run's slice (the same chunk and tile grouping in every variant)."""
+    waves), a 1/2 target shard the double-buffered one, 1/4 and 1/8 shards the
+    mixed grid (3-pair units, then 1-pair units for the last wave) -- with
+    unequal masses (general tile path) the sampled accelerations match the
+    oracle, and every shard is bitwise equal to the full run's slice (the
+    same chunk and tile grouping in every variant)."""
     n = synth.CFG5_N
     pos, vel = synth.nbody_state(n, seed=81)
     pos[:, 3] = (synth.uniform_f32(n, 82, 0.5, 1.5) / n).astype(np.float32)
@@ -406,7 +407,7 @@ def test_nbody_full_size_mixed_masses_and_kernel_variants():
     a_ref = oracle.nbody_accel(pos.astype(np.float64), idx)
     a_gpu = full_v[idx, :3].astype(np.float64) / synth.NBODY_DT
     assert np.max(np.linalg.norm(a_gpu - a_ref, axis=1) / np.linalg.norm(a_ref, axis=1)) <= 1e-4
-    for k, r in ((2, 1), (8, 5)):
+    for k, r in ((2, 1), (4, 2), (8, 5)):
         lo, hi = synth.shard_range(n, r, k)
         v, p = step(lo, hi)
         assert np.array_equal(v, full_v[lo:hi]) and np.array_equal(p, full_p[lo:hi]), (k, r)
