@@ -503,6 +503,24 @@ def paper_protocol(torch, J, reps=3):
         "black_scholes": (300, n24, lambda g, t: g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(t["u"], R),
                                                                                         g.a(t["c"], W), g.a(t["p"], W)]),
                           {"u": pin(synth.bs_rand(n24)), "c": zeros(n24), "p": zeros(n24)}, "P:492"),
+        # the NEXT rows in the same protocol
+        "spmv_bcsstk32_like": (1400, synth.SPMV_N,
+                               lambda g, t: g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(t["rp"], R), g.a(t["col"], R),
+                                                                                g.a(t["val"], R), g.a(t["x"], R),
+                                                                                g.a(t["y"], W)],
+                                                       jacc.jacc_spmv_params_t(synth.SPMV_N, synth.SPMV_N)),
+                               dict(zip(("rp", "col", "val"), map(pin, synth.banded_csr())),
+                                    x=pin(synth.uniform_f32(synth.SPMV_N, 5, -1, 1)), y=zeros(synth.SPMV_N)),
+                               "P:487"),
+        "conv2d_2048_5x5": (300, 2048, lambda g, t: g.add_task(J.JACC_OP_CONV2D_F32, [g.a(t["img"], R),
+                                                                                    g.a(t["f"], R), g.a(t["o"], W)],
+                                                               jacc.jacc_conv2d_params_t(2048, 2048, 2, 0)),
+                            {"img": pin(synth.uniform_f32(2048 * 2048, 11, -1, 1)),
+                             "f": pin(synth.uniform_f32(25, 12, -1, 1)), "o": zeros(2048 * 2048)}, "P:489-490"),
+        "correlation_1024x16384": (1, 1024, lambda g, t: g.add_task(J.JACC_OP_CORR_POPC_U32, [
+            g.a(t["bits"], R), g.a(t["bits"], R), g.a(t["C"], W)], jacc.jacc_corr_params_t(1024, 1024, 512)),
+                                   {"bits": pin(synth.corr_bitsets().view(np.int32)),
+                                    "C": zeros((1024, 1024), torch.int32)}, "P:494"),
     }
     out = {}
     for name, (K, n, one, bufs, cite) in cases.items():
