@@ -71,13 +71,16 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
     if (tid < head) a0 += elem(tid);
     const int64_t n4 = (n - head) / 4;
     int64_t i = tid;
-    for (; i + stride < n4; i += 2 * stride) {
-        float4 u = vec(i), v = vec(i + stride);
+    // 4 vectors in flight per thread (2 left the read stream at ~5.76 TB/s)
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+        const float4 u = vec(i), v = vec(i + stride), w = vec(i + 2 * stride), z = vec(i + 3 * stride);
         a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
         a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+        a0 += w.x; a1 += w.y; a2 += w.z; a3 += w.w;
+        a0 += z.x; a1 += z.y; a2 += z.z; a3 += z.w;
     }
-    if (i < n4) {
-        float4 u = vec(i);
+    for (; i < n4; i += stride) {
+        const float4 u = vec(i);
         a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
     }
     const int64_t t0 = head + 4 * n4;
@@ -109,7 +112,7 @@ size_t reduce_ws_bytes(int64_t) { return sizeof(float) * kMaxGrid + 128; }
 
 namespace {
 void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
-    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, grid, block);
+    pick_grid(s, (n / 4 + kBlock * 4 - 1) / (kBlock * 4), kPerSm, kBlock, grid, block);
     *block = kBlock;   // the block tree assumes kBlock threads
     if (*grid > kMaxGrid) *grid = kMaxGrid;
 }
