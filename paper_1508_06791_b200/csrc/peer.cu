@@ -108,7 +108,7 @@ size_t peer_allreduce_stage_bytes(int64_t n, int, int world) { return peer::allr
 
 cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, cudaStream_t st, int *launches) {
     const int esz = 4;
-    if (n <= 8192) {
+    if (n <= peer::kSmallN) {
         if (is_int)
             allreduce_small_kernel<int><<<1, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (int *)buf, n);
         else

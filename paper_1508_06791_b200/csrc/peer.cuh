@@ -196,11 +196,13 @@ template <typename T> __device__ __forceinline__ T from_bits(uint32_t v);
 template <> __device__ __forceinline__ int from_bits<int>(uint32_t v) { return (int)v; }
 template <> __device__ __forceinline__ float from_bits<float>(uint32_t v) { return __uint_as_float(v); }
 
-// Bytes of staging one allreduce slot needs: 2 epoch parities x world rows
-// of n 8-byte words (the small "LL" form below; the large two-kernel form
-// uses 4-byte rows inside the same area).
+// Allreduces of up to kSmallN elements use the one-block flag-in-data form
+// below (8-byte words); larger ones the two-kernel form (4-byte rows + flags).
+constexpr int64_t kSmallN = 8192;
+
+// Bytes of staging one allreduce slot needs: 2 epoch parities x world rows.
 __host__ __device__ inline size_t allreduce_stage_bytes(int64_t n, int world) {
-    return 2 * (size_t)n * 8 * world;
+    return 2 * (size_t)n * (n <= kSmallN ? 8 : 4) * world;
 }
 
 // Whole block, ONE block of the grid: allreduce-sum of buf[0..n) over all

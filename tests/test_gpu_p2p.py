@@ -162,7 +162,7 @@ def _worker(rank, world, port, q):
         res = {}
         for flags in (0, J.JACC_GRAPH_REPLAY):
             g, _ = make_graph(0, rank=rank, world=world, flags=J.JACC_GRAPH_P2P | flags)
-            peer_setup(g, 16 << 20)
+            peer_setup(g, 32 << 20)
             keys = synth.hist_keys((1 << 20) + 6, seed=31)
             lo, hi = synth.shard_range(keys.size, rank, world)
             x = synth.uniform_f32(200001, 32)
@@ -181,7 +181,9 @@ def _worker(rank, world, port, q):
                 big[:] = bigs[rank]
                 g.run()
                 ref, absum = oracle.reduce_sum(x)
-                big_ref = bigs[0].astype(np.float32) + bigs[1].astype(np.float32)   # rank order, one fp32 add
+                big_ref = bigs[0].astype(np.float32)
+                for r in range(1, world):                    # rank order, fp32 adds
+                    big_ref = big_ref + bigs[r].astype(np.float32)
                 ok[it] = dict(hist=bool(np.array_equal(bins, oracle.histogram(keys, 256))),
                               reduce=bool(abs(s[0] - ref) <= 1e-4 * absum),
                               big=bool(np.array_equal(big, big_ref)),
@@ -202,10 +204,11 @@ def _worker(rank, world, port, q):
         q.put((rank, {"error": traceback.format_exc()}))
 
 
-def test_p2p_world2_one_gpu():
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_world2_one_gpu(world):
+    """world ranks = world processes time-sliced on the box's one GPU."""
     import torch.multiprocessing as mp
-    world = 2
-    port = 29700 + (os.getpid() % 200)
+    port = 29700 + (os.getpid() % 200) + 7 * world
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
