@@ -230,3 +230,43 @@ def test_p2p_world2_one_gpu(world):
             # shard invariance: the 2-rank chain equals the 1-GPU chain bitwise
             assert np.array_equal(ok["pos"], P1[lo:hi]), (r, flags)
             assert np.array_equal(ok["vel"], V1[lo:hi]), (r, flags)
+
+
+def test_p2p_window_errors():
+    """Error paths of the peer windows (include/jacc.h): a full window is
+    JACC_ERR_OOM, handles whose window sizes differ are JACC_ERR_INVALID_ARG
+    (checked before any IPC mapping), a second init is JACC_ERR_STATE."""
+    from paper_1508_06791_b200.torch_glue import make_graph
+    g, _ = make_graph(0, flags=J.JACC_GRAPH_P2P)
+    h = g.peer_init(512 << 10)                 # 256 KiB flag header + 256 KiB heap
+    with pytest.raises(J.JaccError, match="STATE"):
+        g.peer_init(0)
+    assert g.peer_alloc(200 << 10)
+    with pytest.raises(J.JaccError, match="OOM"):
+        g.peer_alloc(200 << 10)
+    g.destroy()
+    g, _ = make_graph(0, rank=0, world=2, flags=J.JACC_GRAPH_P2P)
+    h0 = g.peer_init(1 << 20)
+    h1 = jacc.jacc_peer_handle_t.from_buffer_copy(bytes(h0))
+    h1.rank, h1.window_bytes = 1, 2 << 20
+    with pytest.raises(J.JaccError, match="INVALID_ARG"):
+        g.peer_connect([h0, h1])
+    with pytest.raises(J.JaccError, match="INVALID_ARG"):
+        g.peer_connect([h1, h0])               # handles out of rank order
+    g.destroy()
+
+
+def test_p2p_collective_slot_limit():
+    """Every collective task owns a flag slot; one slot is reserved for the
+    teardown barrier, so a P2P graph takes at most 1023 collective tasks."""
+    from paper_1508_06791_b200.torch_glue import make_graph
+    g, _ = make_graph(0, flags=J.JACC_GRAPH_P2P)
+    x = np.ones(4, np.float32)
+    for _ in range(1023):
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(x, RW)])
+    g.run()
+    assert np.array_equal(x, np.ones(4, np.float32))       # world 1: identity, 1023 times
+    g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(x, RW)])
+    with pytest.raises(J.JaccError, match="UNSUPPORTED"):
+        g.run()
+    g.destroy()
