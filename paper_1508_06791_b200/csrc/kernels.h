@@ -97,6 +97,6 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
 
 // SpMV CSR
 cudaError_t spmv_csr_f32(const int32_t *row_ptr, const int32_t *col, const float *val, const float *x, float *y,
-                         int64_t n, cudaStream_t st, int *launches);
+                         int64_t n, int64_t nnz, cudaStream_t st, int *launches);
 
 }  // namespace jacc_k

@@ -832,7 +832,8 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
         case JACC_OP_SPMV_CSR_F32:
             e = jacc_k::spmv_csr_f32((const int32_t *)P(0), (const int32_t *)P(1), (const float *)P(2),
                                      (const float *)P(3), (float *)P(4),
-                                     ((const jacc_spmv_params_t *)T.params.data())->n, st, launches);
+                                     ((const jacc_spmv_params_t *)T.params.data())->n, (int64_t)a[1].count, st,
+                                     launches);
             break;
         case JACC_OP_ALLREDUCE_SUM:
         case JACC_OP_ALLGATHER:

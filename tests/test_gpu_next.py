@@ -55,8 +55,9 @@ def test_corr_bit_exact(ta, tb, docs):
     assert np.array_equal(C, oracle.corr_popc(A, B))
 
 
+# >= 2^18 rows take the row-block streaming kernel (incl. a ragged last block)
 @pytest.mark.parametrize("n,nnz,bw", [(1, 1, 1), (100, 900, 10), (5000, 100000, 300),
-                                      (synth.SPMV_N, synth.SPMV_NNZ, 1600)])
+                                      (synth.SPMV_N, synth.SPMV_NNZ, 1600), ((1 << 18) + 77, 23 * (1 << 18), 1600)])
 def test_spmv_tolerance(n, nnz, bw):
     rp, col, val = synth.banded_csr(n, nnz, bandwidth=bw, seed=n)
     x = synth.uniform_f32(n, 5, -1, 1)
