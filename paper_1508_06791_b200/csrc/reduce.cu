@@ -112,7 +112,7 @@ size_t reduce_ws_bytes(int64_t) { return sizeof(float) * kMaxGrid + 128; }
 
 namespace {
 void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
-    pick_grid(s, (n / 4 + kBlock * 4 - 1) / (kBlock * 4), kPerSm, kBlock, grid, block);
+    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, grid, block);   // small n: more blocks
     *block = kBlock;   // the block tree assumes kBlock threads
     if (*grid > kMaxGrid) *grid = kMaxGrid;
 }

@@ -1,7 +1,7 @@
 # Round-1 profile capture for the committed evidence (profiles/): launch list and DRAM traffic of the
 # default bench step, ncu --set full of every hot kernel (plain and P2P-fused), bench JSON lines.
 set -x
-TAG=${TAG:-r1e}
+TAG=${TAG:-r1g}
 python -c "import __graft_entry__ as g; g.build()"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_traffic.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > /dev/null 2>&1
