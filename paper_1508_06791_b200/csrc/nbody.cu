@@ -306,37 +306,57 @@ __global__ void __launch_bounds__(kBlock, MINB) nbody_partial_mixed_kernel(const
 // window (rank r's targets at [r n_tgt, (r+1) n_tgt)).  Receivers publish
 // "ready" first: this kernel runs after the step's partial kernel, the last
 // reader of the gathered buffer, and only reads its own slot of it.
+// Four lanes per target: lane q adds the chunk partials of its quarter of
+// the chunks in chunk order, then lane 0 of the quad combines the quarters in
+// a fixed order, ((q0 + q1) + q2) + q3 -- the same function of the partials
+// for every shard size (bitwise shard invariance) with 4x the threads and
+// loads in flight of one lane per target (a 1/8 shard has only 2^14
+// targets: one lane each left the kernel latency-bound).
+constexpr int kFinishLanes = 4;
+
 template <bool kPeer>
 __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restrict__ part, int nchunks,
                                                            const float4 *__restrict__ pos_src, int64_t tgt_offset,
                                                            float4 *__restrict__ vel, float4 *__restrict__ pos_out,
                                                            int64_t n_tgt, float dt, float G, PeerOp pop) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = gt / kFinishLanes;
+    const int q = (int)(gt % kFinishLanes);
     uint64_t e = 0;
     if (kPeer) {
         e = peer::epoch(pop.ctx, pop.slot);
         if (blockIdx.x == 0 && threadIdx.x == 0) peer::signal_all(pop.ctx, peer::kReadyOff, pop.slot, e);
     }
-    float4 np = make_float4(0.f, 0.f, 0.f, 0.f);
+    float3 s3 = make_float3(0.f, 0.f, 0.f);
     if (t < n_tgt) {
-        // chunk partials added in chunk order (the same sum for every shard
-        // size: bitwise shard invariance); loaded 8 at a time so that 8
-        // independent loads are in flight per thread (one at a time made the
-        // kernel latency-bound: 29 us for 128 MiB at 2^17 targets)
+        const int per = (nchunks + kFinishLanes - 1) / kFinishLanes;
+        const int c0 = q * per, c1 = min(nchunks, c0 + per);
         const float4 *pt = part + t;
-        float4 a = __ldg(pt);
-        int c = 1;
-        for (; c + 8 <= nchunks; c += 8) {
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {   // 8 independent loads in flight, added in chunk order
             float4 b[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) b[k] = __ldg(pt + (int64_t)(c + k) * n_tgt);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) { a.x += b[k].x; a.y += b[k].y; a.z += b[k].z; }
+            for (int k = 0; k < 8; ++k) { s3.x += b[k].x; s3.y += b[k].y; s3.z += b[k].z; }
         }
-        for (; c < nchunks; ++c) {
+        for (; c < c1; ++c) {
             const float4 b = __ldg(pt + (int64_t)c * n_tgt);
-            a.x += b.x; a.y += b.y; a.z += b.z;
+            s3.x += b.x; s3.y += b.y; s3.z += b.z;
         }
+    }
+    // quad combine in lane order (all lanes of the warp take part)
+    const unsigned lane = threadIdx.x & 31, base = lane & ~(unsigned)(kFinishLanes - 1);
+    float3 a = s3;
+#pragma unroll
+    for (int k = 1; k < kFinishLanes; ++k) {
+        a.x += __shfl_sync(0xffffffffu, s3.x, base + k);
+        a.y += __shfl_sync(0xffffffffu, s3.y, base + k);
+        a.z += __shfl_sync(0xffffffffu, s3.z, base + k);
+    }
+    float4 np = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool owner = t < n_tgt && q == 0;
+    if (owner) {
         float4 v = vel[t];
         v.x = fmaf(G * a.x, dt, v.x);
         v.y = fmaf(G * a.y, dt, v.y);
@@ -349,9 +369,9 @@ __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restr
     if (!kPeer) return;
     const PeerCtx &c = pop.ctx;
     const size_t slot_off = (size_t)pop.off + ((size_t)c.rank * n_tgt + t) * sizeof(float4);
-    peer::for_each_rank(c, [&](int q, char *b) {
-        if (q != c.rank) peer::block_wait(c, peer::kReadyOff, pop.slot, q, e);
-        if (t < n_tgt) *(float4 *)(b + slot_off) = np;
+    peer::for_each_rank(c, [&](int r, char *b) {
+        if (r != c.rank) peer::block_wait(c, peer::kReadyOff, pop.slot, r, e);
+        if (owner) *(float4 *)(b + slot_off) = np;
     });
     if (!peer::grid_last(c, pop.slot)) return;
     if (threadIdx.x == 0) peer::publish_data(c, pop.slot, e);
@@ -456,7 +476,7 @@ cudaError_t nbody_step_f32(const float4 *pos_src, int64_t n_src, float4 *vel, fl
         ++*launches;
     }
     auto fin = pop ? nbody_finish_kernel<true> : nbody_finish_kernel<false>;
-    fin<<<(unsigned)((n_tgt + 255) / 256), 256, 0, st>>>(part, nchunks > 0 ? (int)nchunks : 1, pos_src,
+    fin<<<(unsigned)((n_tgt * kFinishLanes + 255) / 256), 256, 0, st>>>(part, nchunks > 0 ? (int)nchunks : 1, pos_src,
                                                          p->tgt_offset, vel, pos_out, n_tgt, p->dt, p->G,
                                                          pop ? *pop : PeerOp{});
     ++*launches;
