@@ -106,10 +106,6 @@ typedef enum jacc_dtype {
                                 same pass, bit-identical to the pair); the
                                 action list and counted copies are unchanged,
                                 both tasks report the fused kernel's time   */
-#define JACC_GRAPH_NO_TIMING 32u /* no per-task timing events (jacc_graph_task_ms
-                                then fails with _STATE): for many-task graphs
-                                whose cost is the events, e.g. the paper's
-                                K-iteration protocol (P:502-505)            */
 #define JACC_GRAPH_P2P 16u   /* collectives over NVLink peer memory instead of
                                 NCCL (reading R23): every rank maps the other
                                 ranks' symmetric window (jacc_peer_init /
@@ -125,7 +121,17 @@ typedef enum jacc_dtype {
                                 kernel, no NCCL.  Other collective tasks run
                                 as standalone peer-memory kernels.  Every
                                 rank must build the same graph (SPMD), as for
-                                NCCL; no communicator is needed.            */
+                                NCCL; no communicator is needed.  With
+                                JACC_GRAPH_MERGE as well, vadd -> reduce ->
+                                allreduce is one kernel.  Limits: world <=
+                                JACC_PEER_MAX, 1023 collective tasks per
+                                graph; a peer that never arrives makes the
+                                waiting kernel trap after 30 s (sync then
+                                returns JACC_ERR_CUDA) instead of hanging.  */
+#define JACC_GRAPH_NO_TIMING 32u /* no per-task timing events (jacc_graph_task_ms
+                                then fails with _STATE): for many-task graphs
+                                whose cost is the events, e.g. the paper's
+                                K-iteration protocol (P:502-505)            */
 
 /* -------------------------------------------------------------- ops */
 typedef enum jacc_op {
