@@ -1,6 +1,6 @@
 """Build libjacc.so in-tree with nvcc for sm_100a (no JIT cache, no torch ext).
 
-    python -m paper_1508_06791_b200.build [--force] [-v]
+    python paper_1508_06791_b200/build.py [--force] [-v]   (runs without importing the package)
 
 Every translation unit under csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo`` into build/ and

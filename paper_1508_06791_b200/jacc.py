@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libjacc.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1508_06791_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1508_06791_b200/build.py` "
                       "(there is no CPU or Python fallback)")
 _lib = ctypes.CDLL(LIB_PATH)
 
