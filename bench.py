@@ -539,6 +539,64 @@ def paper_protocol(torch, J, reps=3):
     return out
 
 
+def hist_kiter_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev, K=400):
+    """SURVEY §8(d) at N > 1: the paper's histogram protocol (2^24
+    keys, 256 bins, 400 iterations) as one graph per rank, each iteration
+    counting the rank's key shard and allreducing its bins (fused into the
+    histogram kernel with P2P); alternating bin buffers keep consecutive
+    iterations independent, so an iteration's allreduce can overlap the next
+    one's counting.  Device time per iteration, max over ranks."""
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph, peer_setup
+    R, RW, W = J.JACC_READ, J.JACC_READWRITE, J.JACC_WRITE
+    flags = J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING | (J.JACC_GRAPH_P2P if p2p else 0)
+    g, _ = make_graph(torch.cuda.current_device(), n_streams=2, rank=rank, world=world,
+                      nccl_comm=0 if p2p else comm_ptr, flags=flags)
+    if p2p:
+        peer_setup(g, 8 << 20)
+    n = 1 << 24
+    lo, hi = synth.shard_range(n, rank, world)
+    keys = torch.from_numpy(synth.hist_keys(n)[lo:hi]).cuda()
+    bins = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for k in range(K):
+        g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins[k % 2], W)], jacc.jacc_hist_params_t(256))
+        g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins[k % 2], RW)])
+    g.run()   # capture
+    ts = []
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        comp = g._streams_keep[0]
+        for s_ in comp:
+            s_.wait_event(e0)
+        g.execute()
+        e1.record(comp[0])      # the replayed graph joins every stream into compute[0]
+        g.sync()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = bool(torch.equal(bins[(K - 1) % 2].cpu(), torch.from_numpy(synth_bins_ref())))
+    g.destroy()
+    return {"K": K, "keys": n, "ms_per_graph": float(t.item()), "us_per_iteration": float(t.item()) / K * 1e3,
+            "bins_correct_rank0": ok, "collectives": "p2p (fused into the histogram)" if p2p else "nccl"}
+
+
+_BINS_REF = None
+
+
+def synth_bins_ref():
+    """np.bincount of the 2^24 histogram keys (a check of the K-iteration
+    graph's result, computed with numpy, not the oracle)."""
+    global _BINS_REF
+    if _BINS_REF is None:
+        _BINS_REF = np.bincount(synth.hist_keys(1 << 24), minlength=256).astype(np.int32)
+    return _BINS_REF
+
+
 def _median_run_us(g, reps):
     ts = []
     for _ in range(reps):
@@ -749,6 +807,12 @@ def run_jacc(args):
         hs.g.destroy()
         del hs
 
+    hist_kiter = None
+    if world > 1:
+        try:
+            hist_kiter = hist_kiter_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev)
+        except Exception as exc:
+            hist_kiter = {"error": str(exc)[:300]}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -772,7 +836,7 @@ def run_jacc(args):
                        "compute_streams": 1, "e2e_compute_streams": 4, "plan_replay": bool(args.replay),
                        "sgemm_mode": args.sgemm_mode},
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
-            "e2e": e2e, "step_ms": times, "counted_copies_device_resident": {
+            "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "counted_copies_device_resident": {
                 "h2d": int(stats["h2d_count"]), "d2h": int(stats["d2h_count"])}}
     if world == 1 and not args.no_e2e:
         try:
