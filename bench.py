@@ -813,6 +813,24 @@ def run_jacc(args):
         hs.g.destroy()
         del hs
 
+    # NVLink accounting of the fused collectives (B200_PROFILING.md: a fused
+    # compute + collective kernel's target time is the slower of its compute
+    # roofline and the bytes that must cross NVLink / 770 GB/s per direction)
+    nvlink = None
+    if world > 1:
+        link = 770.0   # GB/s per direction per GPU, measured peer copy (guide)
+        n5 = synth.CFG5_N
+        per = {"allgather_pos (fused into each N-body step)": (world - 1) * (n5 // world) * 16 * synth.CFG5_STEPS,
+               "allreduce_bins (fused into the histogram)": (world - 1) * 256 * 8,
+               "allreduce_s (fused into the reduction)": (world - 1) * 8}
+        nb_ms = statistics.mean(ktimes["nbody"]) if ktimes.get("nbody") else None
+        nvlink = {"link_gbs": link, "per_graph": {k: {"bytes_out_per_rank": v, "min_us": v / link / 1e3}
+                                                 for k, v in per.items()},
+                  "nbody_step_ms": nb_ms,
+                  "nbody_nvlink_share_of_bound": (per["allgather_pos (fused into each N-body step)"] /
+                                                  synth.CFG5_STEPS / link / 1e6) / nb_ms if nb_ms else None,
+                  "note": "the N-body step's bound is its FP32 compute; the all-gather's NVLink time per step is "
+                          "this share of it and overlaps the kick/drift stores"}
     hist_kiter = None
     if world > 1:
         try:
@@ -842,7 +860,8 @@ def run_jacc(args):
                        "compute_streams": 1, "e2e_compute_streams": 4, "plan_replay": bool(args.replay),
                        "sgemm_mode": args.sgemm_mode},
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
-            "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "counted_copies_device_resident": {
+            "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "nvlink": nvlink,
+            "counted_copies_device_resident": {
                 "h2d": int(stats["h2d_count"]), "d2h": int(stats["d2h_count"])}}
     if world == 1 and not args.no_e2e:
         try:
