@@ -381,7 +381,9 @@ __global__ void __launch_bounds__(256) nbody_finish_kernel(const float4 *__restr
 typedef void (*partial_fn)(const float4 *, int64_t, int64_t, int64_t, float, float4 *);
 struct Variant { partial_fn fn; int tpt; };
 
-// Source loop unrolled by 4 (2 and 8 measured slower).  P = 3 pairs (152
+// Source loop unrolled by 4 (re-measured with the equal-mass path, ms per
+// 2^17 step: P3/unroll 4 6.087, unroll 1 6.52, 2 6.20, 8 6.19; P4/2 6.43;
+// P2/8 6.34).  P = 3 pairs (152
 // registers, 6 blocks/SM) is the fastest per interaction at 2^17 bodies
 // (6.54 ms vs 6.67 for P = 2 at 10 blocks/SM, 7.0 for P = 4); P = 2 and
 // P = 1 give more, smaller units when a shard has few targets.  The variant
