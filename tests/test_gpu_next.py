@@ -80,3 +80,45 @@ def test_conv2d_delta_exact(shape):
     out = _conv(img, f)
     ref, _ = oracle.conv2d(img, f)
     assert np.array_equal(out.astype(np.float64), ref)
+
+
+@pytest.mark.slow
+def test_conv2d_roofline_size_sampled_strips():
+    """16384^2 (bench next_rows' roofline point, the TMA kernel): sampled
+    32-row strips -- top edge, bottom edge, interior, ragged tile rows --
+    against the fp64 oracle run on the strip plus its 2-row halos (rows whose
+    5x5 window stays inside the strip equal the full-image result)."""
+    import torch
+    n, r = 16384, 2
+    img = synth.uniform_f32(n * n, 501, -1, 1).reshape(n, n)
+    f = synth.uniform_f32(25, 502, -1, 1).reshape(5, 5)
+    dimg = torch.from_numpy(img).cuda()
+    out = torch.empty_like(dimg)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(dimg, R), g.a(torch.from_numpy(f).cuda(), R), g.a(out, W)],
+               jacc.jacc_conv2d_params_t(n, n, r, 0))
+    g.run()
+    g.destroy()
+    for y0 in (0, 64 * 37 + 5, 8191, n - 32):
+        lo, hi = max(0, y0 - r), min(n, y0 + 32 + r)
+        ref, ab = oracle.conv2d(img[lo:hi], f)
+        got = out[y0:y0 + 32].cpu().numpy().astype(np.float64)
+        ref, ab = ref[y0 - lo:y0 - lo + 32], ab[y0 - lo:y0 - lo + 32]
+        assert np.all(np.abs(got - ref) <= 1e-5 * ab + 1e-30), y0
+
+
+@pytest.mark.slow
+def test_spmv_roofline_size_stream_kernel():
+    """2M rows x 23 non-zeros (bench next_rows' roofline point, the row-block
+    streaming kernel) against the fp64 oracle, every row."""
+    n = 1 << 21
+    rp, col, val = synth.banded_csr(n, 23 * n)
+    x = synth.uniform_f32(n, 503, -1, 1)
+    y = np.zeros(n, np.float32)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(rp, R), g.a(col, R), g.a(val, R), g.a(x, R), g.a(y, W)],
+               jacc.jacc_spmv_params_t(n, n))
+    g.run()
+    g.destroy()
+    ref, ab = oracle.spmv_csr(rp, col, val, x)
+    assert np.all(np.abs(y.astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)
