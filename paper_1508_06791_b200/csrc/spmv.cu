@@ -129,7 +129,10 @@ cudaError_t spmv_csr_f32(const int32_t *row_ptr, const int32_t *col, const float
     // Streaming row blocks for large matrices with short rows; the lane kernel
     // for L2-resident ones (measured, ms: 2M rows x 23 -- lane 0.134, stream
     // 128 rows / 4 loads 0.118, 64 rows 0.121, 256 rows 0.32, 8 loads 0.129;
-    // 44609 rows -- lane 0.0122, stream 0.0135) and for long rows
+    // 44609 rows -- lane 0.0122, stream 0.0135) and for long rows.  The
+    // stream kernel is L1-bound on the x gathers (ncu L1TEX 88.6 %); 16-byte
+    // col/val loads (0.118) and an x window staged in shared memory per block
+    // (0.138-0.16) did not help
     if (n >= (1 << 18) && nnz <= (int64_t)n * (kNnzCap / kRowsPerBlock))
         spmv_stream_kernel<4><<<(unsigned)((n + kRowsPerBlock - 1) / kRowsPerBlock),
                                                          kStreamThreads, 0, st>>>(row_ptr, col, val, x, y, n);
