@@ -12,19 +12,19 @@
 // shared-memory value it loads feeds up to (2r+1) FMAs.
 //
 // TMA path (row stride a multiple of 16 bytes, radius 2 = the paper's 5 x 5):
-// persistent blocks walk 64 x 64 output tiles in row-major order; the 72 x
-// (64 + 2r) input box of each tile (x from x0 - 4, y from y0 - r) arrives by
-// one cp.async.bulk.tensor 2-D load into a 3-stage mbarrier ring, 2 tiles
-// ahead, and TMA's out-of-bounds zero fill IS the zero padding on all four
-// sides.  The box starts 4 columns (16 bytes) left of the tile because the
-// innermost start coordinate must be a multiple of 16 bytes -- measured on
-// the box with scripts/micro/tma_probe.cu: x = -2 or 250 (floats) faults with
-// an illegal instruction, x = -4 / 252 and any row coordinate work, out-of-
-// range parts zero-filled.  Each thread computes a 2 x 4 patch
-// (two x-adjacent outputs, four rows) with the paired FP32 instruction FFMA2
-// -- the two outputs share every filter weight -- and slides down its
-// (2 + 2r)-wide window with 8-byte shared loads, 8 output rows per thread so
-// every loaded row feeds up to 2r + 1 of them; outputs leave as 8-byte
+// persistent blocks walk PX x 64 output tiles in row-major order (PX = 128
+// for large images, 64 when there are few tiles); the (PX + 8) x (64 + 2r)
+// input box of each tile (x from x0 - 4, y from y0 - r) arrives by one
+// cp.async.bulk.tensor 2-D load into an mbarrier ring, and TMA's
+// out-of-bounds zero fill IS the zero padding on all four sides.  The box
+// starts 4 columns (16 bytes) left of the tile because the innermost start
+// coordinate must be a multiple of 16 bytes -- measured on the box with
+// scripts/micro/tma_probe.cu: x = -2 or 250 (floats) faults with an illegal
+// instruction, x = -4 / 252 and any row coordinate work, out-of-range parts
+// zero-filled.  Each thread computes two x-adjacent outputs over QR rows with
+// the paired FP32 instruction FFMA2 (input value broadcast, a pair of filter
+// weights), sliding down its (2 + 2r)-wide window with 8-byte shared loads so
+// every loaded row feeds up to 2r + 1 output rows; outputs leave as 8-byte
 // streaming stores.  Other shapes use the simple kernel below.
 #include "common.cuh"
 #include "kernels.h"
@@ -35,16 +35,27 @@ namespace {
 
 constexpr int TX = 32, TY = 32, Q = 4;     // tile, outputs per thread (rows)
 
-constexpr int PX = 64, PY = 64, kStages = 3;   // TMA path: output tile, ring depth
-constexpr int QR = 8;                          // TMA path: output rows per thread (x 2 columns)
-template <int R>
+// TMA path configurations: output tile PX x 64, QR output rows per thread
+// (x 2 columns, 256 threads), ring depth.  Measured at 16384^2 (ms, same-box
+// A/B): 64 x 64 / QR 8 / 3 stages 0.387, 4 stages 0.388; 128 x 64 / QR 16 /
+// 2 stages 0.367, 3 stages 0.396.  At 2048^2 (512 tiles, L2-resident) the
+// 64-wide tile is faster (16.9 vs 18.7 us): more tiles than blocks.
+template <int PX_, int QR_, int kStages_>
+struct TmaCfg {
+    static constexpr int PX = PX_, PY = 64, QR = QR_, kStages = kStages_;
+    static_assert((PX / 2) * (PY / QR) == 256, "256 threads: PX / 2 column pairs x PY / QR row groups");
+};
+using CfgSmall = TmaCfg<64, 8, 3>;
+using CfgLarge = TmaCfg<128, 16, 2>;
+
+template <int R, class C>
 struct Box {
     static constexpr int X0 = 4;                      // box starts 4 floats (16 B) left of the tile
-    static constexpr int W = PX + 2 * X0;             // 72: covers x0 - 4 .. x0 + 67
-    static constexpr int H = PY + 2 * R;
+    static constexpr int W = C::PX + 2 * X0;          // covers x0 - 4 .. x0 + PX + 3
+    static constexpr int H = C::PY + 2 * R;
     static constexpr int kBytes = W * H * 4;
     static constexpr int kStride = (kBytes + 1023) & ~1023;   // TMA destinations: 128-byte (here 1 KiB) aligned
-    static constexpr int kSmem = kStages * kStride + 1024;    // + alignment slack of the dynamic base
+    static constexpr int kSmem = C::kStages * kStride + 1024; // + alignment slack of the dynamic base
     static_assert(R <= X0 && ((X0 - R) & 1) == 0, "window start must be even (8-byte shared loads)");
 };
 
@@ -52,27 +63,34 @@ __device__ __forceinline__ void st_stream2(float *p, float2 v) {
     asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
-template <int R>
+template <int R, class C>
 __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t H,
                                                             int64_t W, const float *__restrict__ filt,
                                                             float *__restrict__ out, int tiles_x, int ntiles) {
-    constexpr int K = 2 * R + 1, BW = Box<R>::W;
-    constexpr uint32_t kBytes = Box<R>::kBytes;
-    constexpr int kStrideF = Box<R>::kStride / 4;            // floats between ring stages
+    constexpr int K = 2 * R + 1, BW = Box<R, C>::W, PX = C::PX, PY = C::PY, QR = C::QR, kStages = C::kStages;
+    constexpr uint32_t kBytes = Box<R, C>::kBytes;
+    constexpr int kStrideF = Box<R, C>::kStride / 4;         // floats between ring stages
     extern __shared__ uint8_t smem_raw[];
     // kStages boxes, 1 KiB aligned; offset arithmetic on the shared array (not
     // through an integer) keeps the loads below LDS instead of generic LD
     float *ring = reinterpret_cast<float *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
     __shared__ __align__(8) uint64_t bar[kStages];
-    const int tid = threadIdx.x, cx = tid & 31, rg = tid >> 5;   // column pair, row group (QR rows)
-    float2 ff[K * K];                                            // flipped filter, (w, w) pairs
-#pragma unroll
-    for (int m = 0; m < K; ++m)
-#pragma unroll
-        for (int n = 0; n < K; ++n) {
-            const float w = __ldg(filt + (2 * R - m) * K + (2 * R - n));
-            ff[m * K + n] = make_float2(w, w);
-        }
+    const int tid = threadIdx.x, cx = tid % (PX / 2), rg = tid / (PX / 2);   // column pair, row group (QR rows)
+    // Weights of the thread's input column j (j = 0 .. K) in its output pair
+    // (c, c + 1): lo takes w(m, j), hi takes w(m, j - 1), w = the flipped
+    // filter.  Inner columns are one FFMA2 with the input value broadcast to
+    // both halves (no re-pairing of adjacent inputs into operand pairs: that
+    // cost ~8 MOVs per output), the outer two a plain FFMA on one half.  The
+    // (w(m, j), w(m, j - 1)) pairs are built in shared memory and loaded as
+    // pairs, so the compiler keeps 20 pair registers instead of re-pairing 25
+    // scalars with MOVs.  Per output: 10 FFMA2 + 5 FFMA, summed in the same
+    // order as the oracle's definition (filter column by filter column).
+    __shared__ float2 gtab[K * (K - 1)];
+    if (tid < K * (K - 1)) {
+        const int m = tid / (K - 1), j = tid % (K - 1) + 1;
+        gtab[tid] = make_float2(__ldg(filt + (2 * R - m) * K + (2 * R - j)),
+                                __ldg(filt + (2 * R - m) * K + (2 * R - j + 1)));
+    }
     // (the map's address is taken directly in the kernel body: through a
     // capturing lambda nvcc 12.9 passed the wrong parameter slot to UTMALDG)
 #define CONV_ISSUE(t_, stage_)                                                                     \
@@ -80,7 +98,7 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
         const int x0_ = ((t_) % tiles_x) * PX, y0_ = ((t_) / tiles_x) * PY;                       \
         const uint32_t b_ = tc::smem_u32(&bar[(stage_)]);                                          \
         tc::mbar_expect_tx(b_, kBytes);                                                            \
-        tc::tma_load_2d(tc::smem_u32(ring + (stage_) * kStrideF), &map, x0_ - Box<R>::X0, y0_ - R, b_); \
+        tc::tma_load_2d(tc::smem_u32(ring + (stage_) * kStrideF), &map, x0_ - Box<R, C>::X0, y0_ - R, b_); \
     } while (0)
     if (tid == 0) {
         tc::tma_prefetch(&map);
@@ -90,6 +108,9 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
             if (blockIdx.x + i * (int)gridDim.x < ntiles) CONV_ISSUE(blockIdx.x + i * (int)gridDim.x, i);
     }
     __syncthreads();
+    float2 gp[K * (K - 1)];
+#pragma unroll
+    for (int i = 0; i < K * (K - 1); ++i) gp[i] = gtab[i];
     // tile coordinates advanced incrementally (no division per tile)
     const int dtx = (int)gridDim.x % tiles_x, dty = (int)gridDim.x / tiles_x;
     int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
@@ -99,7 +120,7 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
         const int tn = t + (kStages - 1) * gridDim.x;   // refill the stage freed in iteration k - 1
         if (tid == 0 && tn < ntiles) CONV_ISSUE(tn, (k + kStages - 1) % kStages);
         tc::mbar_wait(tc::smem_u32(&bar[stage]), (k / kStages) & 1);
-        const float *S = ring + stage * kStrideF + (rg * QR) * BW + 2 * cx + (Box<R>::X0 - R);
+        const float *S = ring + stage * kStrideF + (rg * QR) * BW + 2 * cx + (Box<R, C>::X0 - R);
         float2 acc[QR];
 #pragma unroll
         for (int q = 0; q < QR; ++q) acc[q] = make_float2(0.f, 0.f);
@@ -117,7 +138,11 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
                 const int m = w - q;
                 if (m < 0 || m > 2 * R) continue;
 #pragma unroll
-                for (int n = 0; n < K; ++n) acc[q] = __ffma2_rn(ff[m * K + n], make_float2(v[n], v[n + 1]), acc[q]);
+                acc[q].x = fmaf(gp[m * (K - 1)].y, v[0], acc[q].x);
+#pragma unroll
+                for (int j = 1; j < K; ++j)
+                    acc[q] = __ffma2_rn(gp[m * (K - 1) + j - 1], make_float2(v[j], v[j]), acc[q]);
+                acc[q].y = fmaf(gp[m * (K - 1) + K - 2].x, v[K], acc[q].y);
             }
         }
         const int64_t xo = (int64_t)tx * PX + 2 * cx, yo = (int64_t)ty * PY + rg * QR;
@@ -179,22 +204,31 @@ __global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ i
     }
 }
 
+template <int R, class C>
+cudaError_t launch_tma_cfg(const float *img, int64_t H, int64_t W, const float *filt, float *out, cudaStream_t st,
+                           bool *done) {
+    *done = false;
+    CUtensorMap map;
+    if (!tc::make_map_2d(&map, img, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, H, W, W * 4, Box<R, C>::H, Box<R, C>::W, 0))
+        return cudaSuccess;   // no tensor map for this shape: the simple kernel runs
+    const int smem = Box<R, C>::kSmem;
+    cudaError_t e = set_max_dyn_smem((const void *)conv2d_tma_kernel<R, C>, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles_x = (W + C::PX - 1) / C::PX, ntiles = tiles_x * ((H + C::PY - 1) / C::PY);
+    int64_t grid = (int64_t)sm_count() * blocks_per_sm((const void *)conv2d_tma_kernel<R, C>, 256, smem);
+    if (grid > ntiles) grid = ntiles;
+    conv2d_tma_kernel<R, C><<<(unsigned)grid, 256, smem, st>>>(map, H, W, filt, out, (int)tiles_x, (int)ntiles);
+    *done = true;
+    return cudaGetLastError();
+}
+
 template <int R>
 cudaError_t launch_tma(const float *img, int64_t H, int64_t W, const float *filt, float *out, cudaStream_t st,
                        bool *done) {
-    *done = false;
-    CUtensorMap map;
-    if (!tc::make_map_2d(&map, img, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, H, W, W * 4, Box<R>::H, Box<R>::W, 0))
-        return cudaSuccess;   // no tensor map for this shape: the simple kernel runs
-    const int smem = Box<R>::kSmem;
-    cudaError_t e = set_max_dyn_smem((const void *)conv2d_tma_kernel<R>, smem);
-    if (e != cudaSuccess) return e;
-    const int64_t tiles_x = (W + PX - 1) / PX, ntiles = tiles_x * ((H + PY - 1) / PY);
-    int64_t grid = (int64_t)sm_count() * blocks_per_sm((const void *)conv2d_tma_kernel<R>, 256, smem);
-    if (grid > ntiles) grid = ntiles;
-    conv2d_tma_kernel<R><<<(unsigned)grid, 256, smem, st>>>(map, H, W, filt, out, (int)tiles_x, (int)ntiles);
-    *done = true;
-    return cudaGetLastError();
+    // the wide tile once there are >= 16 of its tiles per SM (HBM-streaming sizes)
+    const int64_t wide_tiles = ((W + CfgLarge::PX - 1) / CfgLarge::PX) * ((H + CfgLarge::PY - 1) / CfgLarge::PY);
+    if (wide_tiles >= 16 * (int64_t)sm_count()) return launch_tma_cfg<R, CfgLarge>(img, H, W, filt, out, st, done);
+    return launch_tma_cfg<R, CfgSmall>(img, H, W, filt, out, st, done);
 }
 
 }  // namespace
@@ -203,8 +237,8 @@ cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt
                        cudaStream_t st, int *launches) {
     if (H <= 0 || W <= 0) return cudaSuccess;
     // TMA path: 16-byte aligned rows, int32 tile coordinates
-    if (radius == 2 && W % 4 == 0 && aligned16(img) && (W + PX) < (1ll << 31) &&
-        (H + PY) < (1ll << 31) && ((W + PX - 1) / PX) * ((H + PY - 1) / PY) < (1ll << 31)) {
+    if (radius == 2 && W % 4 == 0 && aligned16(img) && (W + 128) < (1ll << 31) &&
+        (H + 64) < (1ll << 31) && ((W + 63) / 64) * ((H + 63) / 64) < (1ll << 31)) {
         bool done = false;
         cudaError_t e = launch_tma<2>(img, H, W, filt, out, st, &done);
         if (e != cudaSuccess) return e;

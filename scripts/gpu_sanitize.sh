@@ -30,6 +30,7 @@ g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(rp, R), g.a(col, R), g.a(val, R), g.a(x,
 # paths added later in round 1: conv2d TMA kernel (W % 4 == 0, radius 2), corr and
 # SGEMM split-K, N-body mixed grid (a 2^14-target shard of 2^16 sources: 1376 3-pair units)
 img2 = synth.uniform_f32(67 * 132, 4).reshape(67, 132); out2 = np.zeros_like(img2)
+img3 = synth.uniform_f32(4736 * 4096, 6).reshape(4736, 4096); out3 = np.zeros_like(img3)   # the 128-wide-tile TMA config (2368 tiles)
 bits2 = synth.corr_bitsets(100, 16384); cc2 = np.zeros((100, 100), np.int32)
 A2, B2 = synth.sgemm_inputs(300, 520, 1000, "signed"); C2 = np.zeros((300, 520), np.float32)
 pos3, vel3 = synth.nbody_state(1 << 16); vel3 = vel3[:1 << 14].copy(); pos4 = np.zeros_like(vel3)
@@ -37,6 +38,7 @@ g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img2, R), g.a(f, R), g.a(out2, W)], jacc.j
 g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits2.view(np.int32), R), g.a(bits2.view(np.int32), R), g.a(cc2, W)], jacc.jacc_corr_params_t(100, 100, 512))
 g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A2, R), g.a(B2, R), g.a(C2, W)], jacc.jacc_sgemm_params_t(300, 520, 1000, 1000, 520, 520, 0, 0))
 g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(pos3, R, f32x4=True), g.a(vel3, RW, f32x4=True), g.a(pos4, W, f32x4=True)], jacc.jacc_nbody_params_t(1 << 14, 0.016, 0.01, 1.0))
+g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img3, R), g.a(f, R), g.a(out3, W)], jacc.jacc_conv2d_params_t(4736, 4096, 2, 0))
 g.run(); g.run()
 print("ok", g.stats()["launches"])
 g.destroy()

@@ -27,11 +27,13 @@ def _conv(img, f):
     return out
 
 
-# TMA path: W % 4 == 0 and r <= 2 (ragged 64 x 32 tiles, tiny images, many
-# tiles per persistent block); the others take the simple kernel
+# TMA path: W % 4 == 0 and r == 2 (ragged 64 x 64 tiles, tiny images, many
+# tiles per persistent block; 4739 x 4100 takes the 128 x 64 tile config,
+# >= 16 tiles per SM, with ragged tiles on both edges); the others take the
+# simple kernel
 @pytest.mark.parametrize("H,Wd,r", [(1, 1, 2), (7, 9, 2), (33, 65, 1), (256, 256, 2), (100, 37, 3),
                                     (64, 64, 4), (2048, 2048, 2), (1, 4, 2), (3, 8, 1), (97, 132, 2),
-                                    (33, 68, 1), (31, 260, 2), (1000, 1028, 2)])
+                                    (33, 68, 1), (31, 260, 2), (1000, 1028, 2), (4739, 4100, 2)])
 def test_conv2d_tolerance(H, Wd, r):
     img = synth.uniform_f32(H * Wd, 100 + H, -1, 1).reshape(H, Wd)
     f = synth.uniform_f32((2 * r + 1) ** 2, 200 + r, -1, 1).reshape(2 * r + 1, 2 * r + 1)
@@ -71,7 +73,7 @@ def test_spmv_tolerance(n, nnz, bw):
     assert np.all(np.abs(y - ref) <= 1e-5 * ab + 1e-30)
 
 
-@pytest.mark.parametrize("shape", [(40, 50), (40, 132)])   # simple kernel / TMA path (zero-filled halo)
+@pytest.mark.parametrize("shape", [(40, 50), (40, 132), (4739, 4100)])   # simple kernel / TMA path (zero-filled halo)
 def test_conv2d_delta_exact(shape):
     f = synth.uniform_f32(25, 3).reshape(5, 5)
     img = np.zeros(shape, np.float32)
