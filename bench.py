@@ -463,7 +463,7 @@ def next_rows(torch, J, peaks, reps=10):
     i8_peak = peaks["bf16_tflops"] * 2
     out["corr_1024x16384"] = {"ms": ms, "achieved": ops / (ms * 1e-3) / 1e12, "unit": "TOPS (u8 MAC = 2)",
                               "peak": i8_peak, "frac": ops / (ms * 1e-3) / 1e12 / i8_peak,
-                              "note": "incl. the two bit-unpack kernels; i8 peak = bf16 x 2 (nominal ratio)"}
+                              "note": "incl. the bit-unpack kernel (A == B: one); i8 peak = bf16 x 2 (nominal ratio)"}
     for v in out.values():
         v["peak_source"] = peaks["source"] + (" (burst: timed alone)" if v["unit"].startswith("TOPS") else "")
     del flush
