@@ -50,33 +50,38 @@ __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + 
 // writes bytes [16 l, 16 l + 16), the expansion of half (l & 1) of word l / 2
 // -- every store instruction is fully coalesced.
 __device__ __forceinline__ uint32_t expand4(uint32_t nib) {   // 4 bits -> 4 bytes (little endian)
-    return (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 | ((nib >> 3) & 1u) << 24;
+    // nib x (1 + 2^7 + 2^14 + 2^21) places copies of the nibble at bits 0, 7,
+    // 14, 21 (no carries: the copies do not overlap); bit k of copy k lands
+    // on bit 8 k
+    return ((nib & 0xFu) * 0x00204081u) & 0x01010101u;
 }
 
-__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t *__restrict__ bits, int64_t t, int64_t words,
-                                                     uint8_t *__restrict__ x, int64_t tp, int64_t kp) {
+template <typename I>   // index type: 32-bit when every index fits (the usual case), else 64-bit
+__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t *__restrict__ bits, I t, I words,
+                                                     uint8_t *__restrict__ x, I tp, I kp) {
     constexpr int U = 4;   // runs per warp per pass: their loads are issued together
     const int lane = threadIdx.x & 31;
-    const int64_t rpr = (kp + 511) / 512;    // kp is a multiple of 128: a row's last run may be partial
-    const int64_t total = tp * rpr;
-    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t q0 = warp0; q0 < total; q0 += U * nwarps) {
+    const I rpr = (kp + 511) / 512;    // kp is a multiple of 128: a row's last run may be partial
+    const I total = tp * rpr;
+    const I warp0 = (I)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const I nwarps = (I)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    for (I q0 = warp0; q0 < total; q0 += U * nwarps) {
         uint32_t v[U];
-        int64_t dst[U];
+        I dst[U];
+        bool ok[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + u * nwarps;
-            const int64_t r = q / rpr, byte = (q - r * rpr) * 512 + 16 * lane, w = byte / 32;
-            const bool ok = q < total && byte < kp;
-            dst[u] = ok ? r * kp + byte : -1;
-            v[u] = (ok && r < t && w < words) ? __ldg(bits + r * words + w) : 0u;
+            const I q = q0 + u * nwarps;
+            const I r = q / rpr, byte = (q - r * rpr) * 512 + 16 * lane, w = byte / 32;
+            ok[u] = q < total && byte < kp;
+            dst[u] = r * kp + byte;
+            v[u] = (ok[u] && r < t && w < words) ? __ldg(bits + (int64_t)r * words + w) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (dst[u] < 0) continue;
+            if (!ok[u]) continue;
             const uint32_t h = (lane & 1) ? v[u] >> 16 : v[u];
-            *(uint4 *)(x + dst[u]) = make_uint4(expand4(h), expand4(h >> 4), expand4(h >> 8), expand4(h >> 12));
+            *(uint4 *)(x + (int64_t)dst[u]) = make_uint4(expand4(h), expand4(h >> 4), expand4(h >> 8), expand4(h >> 12));
         }
     }
 }
@@ -285,14 +290,19 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
     uint8_t *xb = xa + tap * kp;
     const int grid_u = sm_count() * 8;
     const bool same = A == B && ta == tb;   // C = X X^T: one unpacked copy serves both operands
-    unpack_kernel<<<grid_u, 256, 0, st>>>(A, ta, words, xa, same ? tbp : tap, kp);
-    ++*launches;
-    if (same) {
-        xb = xa;
-    } else {
-        unpack_kernel<<<grid_u, 256, 0, st>>>(B, tb, words, xb, tbp, kp);
+    const bool i32 = (tap > tbp ? tap : tbp) * kp < (1ll << 31);
+    auto unpack = [&](const uint32_t *bits, int64_t t, uint8_t *x, int64_t tp) {
+        if (i32)
+            unpack_kernel<int32_t><<<grid_u, 256, 0, st>>>(bits, (int32_t)t, (int32_t)words, x, (int32_t)tp, (int32_t)kp);
+        else
+            unpack_kernel<int64_t><<<grid_u, 256, 0, st>>>(bits, t, words, x, tp, kp);
         ++*launches;
-    }
+    };
+    unpack(A, ta, xa, same ? tbp : tap);
+    if (same)
+        xb = xa;
+    else
+        unpack(B, tb, xb, tbp);
     CUtensorMap ma, mb;
     if (!tc::make_map_2d(&ma, xa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tap, kp, kp, BM, BK, 128) ||
         !tc::make_map_2d(&mb, xb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tbp, kp, kp, BN, BK, 128))
