@@ -124,3 +124,27 @@ def test_spmv_roofline_size_stream_kernel():
     g.destroy()
     ref, ab = oracle.spmv_csr(rp, col, val, x)
     assert np.all(np.abs(y.astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_corr_replayed_graph_bit_exact(same):
+    """corr inside a captured plan (JACC_GRAPH_REPLAY): the GEMM is launched
+    with programmatic stream serialization after the unpack kernel and a
+    (1, 1, splits) cluster -- both must survive stream capture.  Replayed
+    three times with new bitsets between runs (the host buffers are re-read
+    every execute), each result bit-exact."""
+    g, _ = make_graph(0, flags=J.JACC_GRAPH_REPLAY)
+    A = synth.corr_bitsets(1024, 16384, 0.5, seed=11)
+    B = A if same else synth.corr_bitsets(300, 16384, 0.3, seed=12)
+    C = np.zeros((1024, B.shape[0]), np.int32)
+    g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(A.view(np.int32), R), g.a(B.view(np.int32), R), g.a(C, W)],
+               jacc.jacc_corr_params_t(1024, B.shape[0], 512))
+    for it in range(3):
+        if it:
+            A[:] = synth.corr_bitsets(1024, 16384, 0.5, seed=11 + 7 * it)
+            if not same:
+                B[:] = synth.corr_bitsets(300, 16384, 0.3, seed=12 + 7 * it)
+        g.run()
+        assert np.array_equal(C, oracle.corr_popc(A, B)), it
+    assert g.stats()["graph_replays"] >= 1
+    g.destroy()
