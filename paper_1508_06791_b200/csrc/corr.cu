@@ -110,6 +110,9 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {   // all threads of every CTA in the cluster
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_sync_relaxed() {   // ordering only: nothing is published
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 __device__ __forceinline__ int4 ld_dsmem_v4(uint32_t local_addr, uint32_t rank) {
     uint32_t a;
     int4 v;
@@ -126,6 +129,7 @@ __device__ __forceinline__ int4 ld_dsmem_v4(uint32_t local_addr, uint32_t rank) 
 // in split order, and stores them to C.  Row stride 260 words: the epilogue's
 // 16-byte stores of 32 rows hit 8 distinct 16-byte bank groups per wavefront.
 constexpr int kTileStride = BN + 4;
+constexpr int kMaxSplits = 8;   // a portable cluster
 static_assert(BM * kTileStride * 4 <= kStages * kStageBytes, "partial tile fits in the ring");
 
 // C tile (m_blk, n_blk) over K blocks [kb0, kb1).  ldc = tb and bounds
@@ -137,7 +141,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                    int32_t *__restrict__ C, int64_t ta, int64_t tb, int num_kb, int32_t *__restrict__ part,
                    int64_t tap, int64_t tbp, int csum) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1 KiB aligned by offset arithmetic on the shared array (through an integer
+    // the compiler loses the address space: generic stores in the epilogue)
+    uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *bars = (uint64_t *)(smem + kStages * kStageBytes);
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 1);
     const uint32_t full0 = tc::smem_u32(bars), empty0 = tc::smem_u32(bars + kStages),
@@ -228,25 +234,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r0 = rank * BM / S, r1 = (rank + 1) * BM / S;
         const uint32_t tile = tc::smem_u32(smem);
         const bool vec = (tb & 3) == 0 && (((uintptr_t)C) & 15) == 0;
-        for (int it = threadIdx.x; it < (r1 - r0) * (BN / 4); it += kThreads) {
-            const int lr = r0 + it / (BN / 4), lc = (it % (BN / 4)) * 4;
-            const uint32_t off = (uint32_t)(lr * kTileStride + lc) * 4;
-            int4 acc = ld_dsmem_v4(tile + off, 0);
-            for (int sp = 1; sp < S; ++sp) {
-                const int4 v = ld_dsmem_v4(tile + off, (uint32_t)sp);
-                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        // 2 items per thread per pass, all S DSMEM loads of both issued before
+        // any add (a load-add chain per split cost ~4 DSMEM round trips per item)
+        const int nitems = (r1 - r0) * (BN / 4);
+        for (int it0 = threadIdx.x; it0 < nitems; it0 += 2 * kThreads) {
+            int4 v[2][kMaxSplits];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int it = it0 + u * kThreads;
+                const uint32_t off = (uint32_t)((r0 + it / (BN / 4)) * kTileStride + (it % (BN / 4)) * 4) * 4;
+#pragma unroll
+                for (int sp = 0; sp < kMaxSplits; ++sp)
+                    if (it < nitems && sp < S) v[u][sp] = ld_dsmem_v4(tile + off, (uint32_t)sp);
             }
-            const int64_t row = (int64_t)m_blk * BM + lr, col = (int64_t)n_blk * BN + lc;
-            if (row >= ta || col >= tb) continue;
-            int32_t *c = C + row * tb + col;
-            if (vec) {
-                *(int4 *)c = acc;
-            } else {
-                const int32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
-                for (int k = 0; k < 4 && col + k < tb; ++k) c[k] = a4[k];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int it = it0 + u * kThreads;
+                if (it >= nitems) continue;
+                int4 acc = v[u][0];
+#pragma unroll
+                for (int sp = 1; sp < kMaxSplits; ++sp)
+                    if (sp < S) {
+                        acc.x += v[u][sp].x; acc.y += v[u][sp].y; acc.z += v[u][sp].z; acc.w += v[u][sp].w;
+                    }
+                const int lr = r0 + it / (BN / 4), lc = (it % (BN / 4)) * 4;
+                const int64_t row = (int64_t)m_blk * BM + lr, col = (int64_t)n_blk * BN + lc;
+                if (row >= ta || col >= tb) continue;
+                int32_t *c = C + row * tb + col;
+                if (vec) {
+                    *(int4 *)c = acc;
+                } else {
+                    const int32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+                    for (int k = 0; k < 4 && col + k < tb; ++k) c[k] = a4[k];
+                }
             }
         }
-        cluster_sync();   // no CTA leaves while a peer still reads its tile
+        cluster_sync_relaxed();   // no CTA leaves while a peer still reads its tile (loads done)
     }
 }
 
@@ -278,7 +301,7 @@ int corr_splits(int64_t ta, int64_t tb, int64_t words) {
     const int64_t num_kb = round_up(words * 32 > 0 ? words * 32 : 1, BK) / BK;
     int64_t s = sm_count() / (tiles > 0 ? tiles : 1);
     if (s > num_kb / 8) s = num_kb / 8;
-    return (int)(s < 1 ? 1 : s > 8 ? 8 : s);   // <= 8: a portable cluster
+    return (int)(s < 1 ? 1 : s > kMaxSplits ? kMaxSplits : s);   // a portable cluster
 }
 
 }  // namespace
@@ -335,9 +358,7 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;   // the occupancy query takes the cluster shape only
-        int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, (const void *)corr_i8_kernel, &cfg) == cudaSuccess &&
-            clusters > 0) {
+        if (max_active_clusters((const void *)corr_i8_kernel, &cfg) > 0) {   // cached per shape
             cfg.numAttrs = 2;
             e = cudaLaunchKernelEx(&cfg, corr_i8_kernel, (CUtensorMap)ma, (CUtensorMap)mb, C, ta, tb, (int)(kp / BK),
                                    (int32_t *)nullptr, tap, tbp, 1);
@@ -345,7 +366,6 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
             if (e != cudaSuccess) return e;
             return cudaGetLastError();
         }
-        (void)cudaGetLastError();
     }
     int32_t *part = nullptr;
     if (splits > 1)

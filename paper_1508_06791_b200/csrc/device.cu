@@ -54,4 +54,28 @@ int blocks_per_sm(const void *kernel, int block, int dyn_smem) {
     return occ;
 }
 
+int max_active_clusters(const void *kernel, const cudaLaunchConfig_t *cfg) {
+    // key: kernel, device, block, dynamic smem, cluster shape (the grid does not change the answer)
+    static std::map<std::tuple<const void *, int, unsigned, size_t, unsigned, unsigned, unsigned>, int> cache;
+    unsigned cx = 1, cy = 1, cz = 1;
+    for (unsigned i = 0; i < cfg->numAttrs; ++i)
+        if (cfg->attrs[i].id == cudaLaunchAttributeClusterDimension) {
+            cx = cfg->attrs[i].val.clusterDim.x;
+            cy = cfg->attrs[i].val.clusterDim.y;
+            cz = cfg->attrs[i].val.clusterDim.z;
+        }
+    const auto key = std::make_tuple(kernel, current_device(), cfg->blockDim.x * cfg->blockDim.y * cfg->blockDim.z,
+                                     cfg->dynamicSmemBytes, cx, cy, cz);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
+}
+
 }  // namespace jacc_k

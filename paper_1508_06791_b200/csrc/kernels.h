@@ -34,6 +34,9 @@ int sm_count();   // SMs of the current device (148 on B200), cached per device
 cudaError_t set_max_dyn_smem(const void *kernel, int bytes);
 // resident blocks per SM of `kernel` at `block` threads on the current device
 int blocks_per_sm(const void *kernel, int block, int dyn_smem);
+// cudaOccupancyMaxActiveClusters for a launch config (only its cluster attribute, block and
+// dynamic smem matter), cached; 0 when no such cluster can be resident or the query fails
+int max_active_clusters(const void *kernel, const cudaLaunchConfig_t *cfg);
 
 // c = a + b
 cudaError_t vadd_f32(const float *a, const float *b, float *c, int64_t n,
