@@ -132,6 +132,49 @@ constexpr int kTileStride = BN + 4;
 constexpr int kMaxSplits = 8;   // a portable cluster
 static_assert(BM * kTileStride * 4 <= kStages * kStageBytes, "partial tile fits in the ring");
 
+// Rows [r0, r1) of the cluster's S partial tiles, summed in split order into
+// C.  DSMEM loads are latency-bound (~1 us under this load): every thread
+// issues the S loads of kU items before adding any (24 KB in flight per SM
+// with 2 items took 4.6 us for a 1024^2 output; a load-add chain per split
+// was slower still).
+template <int S>
+__device__ __forceinline__ void cluster_sum(uint32_t tile, int r0, int r1, int m_blk, int n_blk, int32_t *C,
+                                            int64_t ta, int64_t tb, bool vec) {
+    constexpr int kU = S <= 4 ? 4 : 2;
+    const int nitems = (r1 - r0) * (BN / 4);
+    for (int it0 = threadIdx.x; it0 < nitems; it0 += kU * kThreads) {
+        int4 v[kU][S];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            const uint32_t off = (uint32_t)((r0 + it / (BN / 4)) * kTileStride + (it % (BN / 4)) * 4) * 4;
+#pragma unroll
+            for (int sp = 0; sp < S; ++sp)
+                if (it < nitems) v[u][sp] = ld_dsmem_v4(tile + off, (uint32_t)sp);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            if (it >= nitems) continue;
+            int4 acc = v[u][0];
+#pragma unroll
+            for (int sp = 1; sp < S; ++sp) {
+                acc.x += v[u][sp].x; acc.y += v[u][sp].y; acc.z += v[u][sp].z; acc.w += v[u][sp].w;
+            }
+            const int lr = r0 + it / (BN / 4), lc = (it % (BN / 4)) * 4;
+            const int64_t row = (int64_t)m_blk * BM + lr, col = (int64_t)n_blk * BN + lc;
+            if (row >= ta || col >= tb) continue;
+            int32_t *c = C + row * tb + col;
+            if (vec) {
+                *(int4 *)c = acc;
+            } else {
+                const int32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+                for (int k = 0; k < 4 && col + k < tb; ++k) c[k] = a4[k];
+            }
+        }
+    }
+}
+
 // C tile (m_blk, n_blk) over K blocks [kb0, kb1).  ldc = tb and bounds
 // checks when writing C directly; a padded [tap x tbp] partial (split
 // blockIdx.z) when `part` is set; summed over the cluster's DSMEM when
@@ -234,40 +277,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r0 = rank * BM / S, r1 = (rank + 1) * BM / S;
         const uint32_t tile = tc::smem_u32(smem);
         const bool vec = (tb & 3) == 0 && (((uintptr_t)C) & 15) == 0;
-        // 2 items per thread per pass, all S DSMEM loads of both issued before
-        // any add (a load-add chain per split cost ~4 DSMEM round trips per item)
-        const int nitems = (r1 - r0) * (BN / 4);
-        for (int it0 = threadIdx.x; it0 < nitems; it0 += 2 * kThreads) {
-            int4 v[2][kMaxSplits];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int it = it0 + u * kThreads;
-                const uint32_t off = (uint32_t)((r0 + it / (BN / 4)) * kTileStride + (it % (BN / 4)) * 4) * 4;
-#pragma unroll
-                for (int sp = 0; sp < kMaxSplits; ++sp)
-                    if (it < nitems && sp < S) v[u][sp] = ld_dsmem_v4(tile + off, (uint32_t)sp);
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int it = it0 + u * kThreads;
-                if (it >= nitems) continue;
-                int4 acc = v[u][0];
-#pragma unroll
-                for (int sp = 1; sp < kMaxSplits; ++sp)
-                    if (sp < S) {
-                        acc.x += v[u][sp].x; acc.y += v[u][sp].y; acc.z += v[u][sp].z; acc.w += v[u][sp].w;
-                    }
-                const int lr = r0 + it / (BN / 4), lc = (it % (BN / 4)) * 4;
-                const int64_t row = (int64_t)m_blk * BM + lr, col = (int64_t)n_blk * BN + lc;
-                if (row >= ta || col >= tb) continue;
-                int32_t *c = C + row * tb + col;
-                if (vec) {
-                    *(int4 *)c = acc;
-                } else {
-                    const int32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
-                    for (int k = 0; k < 4 && col + k < tb; ++k) c[k] = a4[k];
-                }
-            }
+        switch (S) {   // the split count as a constant: every load of a pass in flight at once
+            case 2: cluster_sum<2>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            case 3: cluster_sum<3>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            case 4: cluster_sum<4>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            case 5: cluster_sum<5>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            case 6: cluster_sum<6>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            case 7: cluster_sum<7>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            default: cluster_sum<8>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
         }
         cluster_sync_relaxed();   // no CTA leaves while a peer still reads its tile (loads done)
     }
