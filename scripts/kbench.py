@@ -37,7 +37,8 @@ def main():
     from paper_1508_06791_b200.torch_glue import make_graph, peer_tensor
     R, W, RW = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
     dev = torch.device("cuda", 0)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    from bench import L2Flush   # write + read flush: clean L2 lines (bench.py)
+    flush = L2Flush(torch, dev)
     for op in a.ops:
         g, _ = make_graph(0, n_streams=1, flags=J.JACC_GRAPH_P2P if a.p2p else 0)
         keep = []
