@@ -79,9 +79,14 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict_
         a0 += w.x; a1 += w.y; a2 += w.z; a3 += w.w;
         a0 += z.x; a1 += z.y; a2 += z.z; a3 += z.w;
     }
-    for (; i < n4; i += stride) {
+    if (i < n4) {   // the remainder (< 4 vectors): loads issued together, added in index order
+        const bool h1 = i + stride < n4, h2 = i + 2 * stride < n4;
         const float4 u = vec(i);
+        const float4 v = h1 ? vec(i + stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 w = h2 ? vec(i + 2 * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
         a0 += u.x; a1 += u.y; a2 += u.z; a3 += u.w;
+        if (h1) { a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w; }
+        if (h2) { a0 += w.x; a1 += w.y; a2 += w.z; a3 += w.w; }
     }
     const int64_t t0 = head + 4 * n4;
     if (tid < n - t0) a1 += elem(t0 + tid);

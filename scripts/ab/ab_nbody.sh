@@ -12,7 +12,7 @@ run() {  # $1 = repo copy, $2 = label
 V=("$@"); n=${#V[@]}
 for i in $(seq 0 $((n-1))); do
   d=/tmp/ab_$i; rm -rf $d; mkdir -p $d
-  cp -r $R/paper_1508_06791_b200 $R/scripts $R/synth $R/include $d/
+  cp -r $R/paper_1508_06791_b200 $R/scripts $R/synth $R/include $R/bench.py $d/
   cp ${V[$i]} $d/paper_1508_06791_b200/csrc/nbody.cu
   (cd $d && python -m paper_1508_06791_b200.build > /dev/null)
 done

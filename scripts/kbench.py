@@ -25,6 +25,7 @@ def main():
     ap.add_argument("ops", nargs="+")
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--no-flush", action="store_true", help="no L2 flush between reps (warm L2 / back-to-back)")
     ap.add_argument("--mode", default="3xtf32")
     ap.add_argument("--shards", type=int, default=1, help="nbody: time rank 0's target shard of N/shards bodies")
     ap.add_argument("--p2p", action="store_true",
@@ -117,7 +118,8 @@ def main():
             raise SystemExit(f"unknown op {op}")
         ms = []
         for i in range(a.reps + 2):
-            flush.fill_(1.0)
+            if not a.no_flush:
+                flush.fill_(1.0)
             torch.cuda.synchronize()
             g.run()
             if i >= 2:
