@@ -34,9 +34,19 @@ __global__ void __launch_bounds__(256) vadd_v4_kernel(const float4 *__restrict__
             st_stream(c + i + u * stride, make_float4(x[u].x + y[u].x, x[u].y + y[u].y, x[u].z + y[u].z,
                                                       x[u].w + y[u].w));
     }
-    for (; i < n4; i += stride) {
-        float4 x = ld_stream(a + i), y = ld_stream(b + i);
-        st_stream(c + i, make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w));
+    if (i < n4) {   // the remainder (< kUnroll vectors): loads issued together
+        float4 x[kUnroll - 1], y[kUnroll - 1];
+#pragma unroll
+        for (int u = 0; u < kUnroll - 1; ++u)
+            if (i + u * stride < n4) {
+                x[u] = ld_stream(a + i + u * stride);
+                y[u] = ld_stream(b + i + u * stride);
+            }
+#pragma unroll
+        for (int u = 0; u < kUnroll - 1; ++u)
+            if (i + u * stride < n4)
+                st_stream(c + i + u * stride,
+                          make_float4(x[u].x + y[u].x, x[u].y + y[u].y, x[u].z + y[u].z, x[u].w + y[u].w));
     }
     // the (< 4) trailing scalars
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
