@@ -329,55 +329,131 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
 
 
 # ------------------------------------------------------------ CPU oracle baseline
-def cpu_oracle_sample(scale=1.0):
-    """Time the oracle (as it stands) on a bounded sample of one suite graph;
-    return (extrapolated seconds per full graph, description, threads)."""
-    import oracle
-    t = {}
-    n = synth.CFG1_N
-    a, b = synth.vadd_inputs(n)
-    t0 = time.perf_counter(); c = oracle.vadd(a, b); oracle.reduce_sum(c); t["cfg1"] = (time.perf_counter() - t0, 1.0)
-    nk = int((1 << 24) * scale)
-    keys = synth.hist_keys(nk)
-    t0 = time.perf_counter(); oracle.histogram(keys, 256); t["cfg2"] = (time.perf_counter() - t0, synth.CFG2_N / nk)
-    nb = int((1 << 22) * scale)
-    u = synth.bs_rand(nb)
-    t0 = time.perf_counter(); oracle.blackscholes(u); t["cfg3"] = (time.perf_counter() - t0, synth.CFG3_N / nb)
-    n4 = synth.CFG4_MNK
-    rows = max(1, int(16 * scale))
-    A, B = synth.sgemm_inputs(rows, n4, n4)
-    t0 = time.perf_counter(); oracle.sgemm_rows(A, B); t["cfg4"] = (time.perf_counter() - t0, n4 / rows)
-    pos, vel = synth.nbody_state(synth.CFG5_N)
-    ntg = max(1, int(256 * scale))
-    tg = np.arange(ntg)
-    p64 = pos.astype(np.float64)
-    t0 = time.perf_counter(); oracle.nbody_accel(p64, tg)
-    t["cfg5"] = (time.perf_counter() - t0, synth.CFG5_N / ntg * synth.CFG5_STEPS)
-    total = sum(x * s for x, s in t.values())
-    desc = (f"oracle on host cores: cfg1 full 2^20; cfg2 {nk} keys; cfg3 {nb} options; cfg4 {rows} rows of "
-            f"8192x8192x8192; cfg5 {ntg} targets x 2^17 sources x 1 step; each scaled linearly to the full graph")
-    return total, desc, oracle.num_threads(), {k: v[0] * v[1] for k, v in t.items()}
+def _host_info():
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["model"] = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return info
+
+
+class CpuSample:
+    """One bounded sample of the jacc-suite graph for the CPU oracle (as it
+    stands, never tuned for this), used IDENTICALLY by the --impl reference
+    arm (every step) and the cpu_baseline leg, so the two agree.
+
+    cfg1 (2^20), cfg2 (2^28 keys) and cfg3 (2^26 options) run at FULL size;
+    cfg4 runs 2 x threads rows of the 8192^3 product (each thread gets two
+    whole rows) and cfg5 16 x threads targets of one 2^17-body step; those two
+    are scaled linearly to the full graph (flagged "extrapolated").  The
+    oracle's vadd / reduce / histogram loops are single-threaded, the
+    Black-Scholes, SGEMM and N-body loops use OpenMP over independent outer
+    indices: each part reports the threads it used.  Inputs are generated
+    once, outside the timed calls."""
+
+    def __init__(self, threads=None):
+        import oracle
+        self.oracle = oracle
+        self.threads = threads or oracle.num_threads()
+        oracle.set_num_threads(self.threads)
+        self.a, self.b = synth.vadd_inputs()
+        self.keys = synth.hist_keys()
+        self.u = synth.bs_rand()
+        n4 = synth.CFG4_MNK
+        self.rows = 2 * self.threads
+        self.A, self.B = synth.sgemm_inputs(self.rows, n4, n4)
+        pos, _ = synth.nbody_state(synth.CFG5_N)
+        self.p64 = pos.astype(np.float64)
+        self.ntg = 16 * self.threads
+
+    def run(self, threads=None, small=False):
+        """{part: {"s": measured seconds, "scale": factor to the full graph,
+        "threads": t, "extrapolated": bool}}; small=True shrinks the
+        parallel parts (single-thread timing)."""
+        o = self.oracle
+        T = threads or self.threads
+        o.set_num_threads(T)
+        t = {}
+
+        def timed(name, fn, scale, thr, extra):
+            t0 = time.perf_counter()
+            fn()
+            t[name] = {"s": time.perf_counter() - t0, "scale": scale, "threads": thr, "extrapolated": extra}
+
+        timed("cfg1", lambda: o.reduce_sum(o.vadd(self.a, self.b)), 1.0, 1, False)
+        timed("cfg2", lambda: o.histogram(self.keys, 256), 1.0, 1, False)
+        nb = self.u.size // 16 if small else self.u.size
+        timed("cfg3", lambda: o.blackscholes(self.u[:nb]), self.u.size / nb, T, small)
+        rows = 1 if small else self.rows
+        timed("cfg4", lambda: o.sgemm_rows(self.A[:rows], self.B), synth.CFG4_MNK / rows, T, True)
+        ntg = 16 if small else self.ntg
+        timed("cfg5", lambda: o.nbody_accel(self.p64, np.arange(ntg)), synth.CFG5_N / ntg * synth.CFG5_STEPS,
+              T, True)
+        o.set_num_threads(self.threads)
+        return t
+
+    @staticmethod
+    def total(parts):
+        return sum(v["s"] * v["scale"] for v in parts.values())
+
+    def describe(self):
+        return (f"oracle on the host cores, per step: cfg1 full 2^20 (1 thread); cfg2 full 2^28 keys (1 thread); "
+                f"cfg3 full 2^26 options ({self.threads} threads); cfg4 {self.rows} rows of 8192x8192x8192 "
+                f"({self.threads} threads, x{synth.CFG4_MNK // self.rows} extrapolated); cfg5 {self.ntg} targets "
+                f"x 2^17 sources x 1 step ({self.threads} threads, x{synth.CFG5_N // self.ntg * synth.CFG5_STEPS} "
+                f"extrapolated to 2^17 targets x 10 steps)")
 
 
 def run_reference(args):
     rank, local, world = dist_env()
     if rank != 0:
         return 0
-    steps = []
+    cs = CpuSample()
+    steps, parts = [], None
     for i in range(args.warmup + args.steps):
-        total, desc, cores, parts = cpu_oracle_sample(scale=0.25)
+        p = cs.run()
         if i >= args.warmup:
-            steps.append(total)
+            steps.append(CpuSample.total(p))
+            parts = p
     sec = statistics.mean(steps)
     v = 1.0 / sec
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seeded)", "impl": "reference",
             "config": {"workload": WORKLOAD},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cs.threads, "kind": "oracle",
+                             "sample": cs.describe(), "host": _host_info(),
+                             "parts_s_full_graph": {k: x["s"] * x["scale"] for k, x in parts.items()},
+                             "parts": parts},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_leg():
+    """The cpu_baseline object of the main arm: the same CpuSample as the
+    reference arm (one warm-up + two timed samples, all cores), plus the
+    parallel parts re-timed on ONE thread on a smaller sample."""
+    cs = CpuSample()
+    cs.run()
+    runs = [cs.run() for _ in range(2)]
+    total = statistics.mean(CpuSample.total(p) for p in runs)
+    st = cs.run(threads=1, small=True)
+    return {"value": 1.0 / total, "unit": UNIT, "cores": cs.threads, "kind": "oracle", "sample": cs.describe(),
+            "host": _host_info(), "s_per_graph": total,
+            "parts_s_full_graph": {k: x["s"] * x["scale"] for k, x in runs[-1].items()},
+            "parts": runs[-1],
+            "single_thread": {"s_per_graph": CpuSample.total(st),
+                              "parts_s_full_graph": {k: x["s"] * x["scale"] for k, x in st.items()},
+                              "sample": "cfg1, cfg2 as above; cfg3 2^22 options, cfg4 1 row, cfg5 16 targets; 1 thread"}}
 
 
 # ------------------------------------------------------------ main arm
@@ -733,10 +809,20 @@ def _p2p_probe(torch, J, dist, rank, world, red_dev="cuda"):
     return err
 
 
+def _pci_bus_id(torch):
+    try:
+        p = torch.cuda.get_device_properties(torch.cuda.current_device())
+        return f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}"
+    except Exception:
+        return None
+
+
 def run_jacc(args):
     import torch
     import torch.distributed as dist
     rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
     # JACC_BENCH_SHARED_GPU=1 (testing only, never a bench number): every rank
     # on cuda:0 with a gloo process group, collectives over the P2P windows --
     # exercises the whole N>1 code path on a one-GPU box.
@@ -757,6 +843,14 @@ def run_jacc(args):
     import paper_1508_06791_b200 as J
     from paper_1508_06791_b200 import jacc
     peaks = _peaks()
+    # the ranks that actually ran (one record per process: its CUDA device)
+    me = {"rank": rank, "local_rank": local, "device": torch.cuda.current_device(),
+          "name": torch.cuda.get_device_name(), "pci_bus_id": _pci_bus_id(torch)}
+    if world > 1:
+        ranks_seen = [None] * world
+        dist.all_gather_object(ranks_seen, me)
+    else:
+        ranks_seen = [me]
 
     p2p_note = None
     if world > 1 and args.comm == "p2p":
@@ -876,6 +970,7 @@ def run_jacc(args):
                        "collectives": None if world == 1 else args.comm + (f" ({p2p_note})" if p2p_note else ""),
                        "compute_streams": 1, "e2e_compute_streams": 4, "plan_replay": bool(args.replay),
                        "sgemm_mode": args.sgemm_mode},
+            "nranks": len(ranks_seen), "ranks": ranks_seen,
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
             "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "nvlink": nvlink,
             "counted_copies_device_resident": {
@@ -895,13 +990,24 @@ def run_jacc(args):
         except Exception as exc:
             line["paper_protocol"] = {"error": str(exc)[:300]}
     if not args.no_cpu_baseline and world == 1:
-        total, desc, cores, parts = cpu_oracle_sample()
-        line["cpu_baseline"] = {"value": 1.0 / total, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                "sample": desc, "extrapolated_s_per_graph": total, "parts_s": parts}
+        line["cpu_baseline"] = cpu_baseline_leg()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def relaunch_cmd(argv, gpus, port=None):
+    """`python bench.py --gpus N ...` without a torchrun environment: the
+    command that re-runs this script as N ranks (one process per GPU) under
+    torch.distributed.run, rendezvous on 127.0.0.1."""
+    if port is None:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
 
 
 def main():
@@ -918,6 +1024,12 @@ def main():
     ap.add_argument("--no-replay", dest="replay", action="store_false",
                     help="issue every action from the host each step instead of replaying the captured plan")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run under torchrun instead of silently
+        # measuring one rank (the N-rank launch is the contract's)
+        cmd = relaunch_cmd(sys.argv[1:], args.gpus)
+        print("bench.py: relaunching as " + " ".join(cmd[1:6]), file=sys.stderr, flush=True)
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_jacc(args)

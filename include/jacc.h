@@ -359,6 +359,13 @@ int jacc_graph_stats(const jacc_graph_t *g, jacc_stats_t *out);
  * Errors: _NOT_FOUND, _STATE (no completed execute).                     */
 int jacc_graph_task_ms(const jacc_graph_t *g, int task_id, float *ms);
 
+/* Test hook: change the graph's jacc_config_t.fail_task between executes
+ * (0 = off; k > 0 makes issuing task k-1 fail with JACC_ERR_INJECTED), so a
+ * test can fail one execute and then run the same graph again (R8: a failed
+ * execute leaves host buffers untouched and drops every device residency).
+ * Errors: _INVALID_ARG (k < 0), _STATE (EXECUTING).                      */
+int jacc_graph_set_fail_task(jacc_graph_t *g, int32_t fail_task);
+
 /* Plan (without executing) and write a stable text dump of the edges and
  * the lowered action list (golden tests; cf. SPEC --dump-actions S:460).
  * Writes at most cap bytes (NUL-terminated); *needed = full size + 1.

@@ -57,6 +57,7 @@ def lib():
             build()
             L = ctypes.CDLL(_LIB)
             L.oracle_num_threads.restype = ctypes.c_int
+            L.oracle_set_num_threads.argtypes = [ctypes.c_int]
             L.oracle_vadd_f32.argtypes = [_F32P, _F32P, _F32P, _i64]
             L.oracle_reduce_sum_f32.argtypes = [_F32P, _i64, _f64, ctypes.POINTER(_f64)]
             L.oracle_reduce_sum_f32.restype = _f64
@@ -82,6 +83,11 @@ def lib():
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the parallel oracle loops (results do not depend on it)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 def _c(x, dt):

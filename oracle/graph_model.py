@@ -146,18 +146,6 @@ def counts(actions):
     return c
 
 
-def resident_after(tasks, resident=None):
-    """Buffers whose device copy is current after an execute AND may stay
-    resident (CACHABLE, not DEVICE).  Every buffer a graph touches is current
-    on the device at the end of an execute; only CACHABLE ones are kept."""
-    out = set()
-    for t in tasks:
-        for a in t.args:
-            if a.cachable and not a.device:
-                out.add(a.buf)
-    return out
-
-
 # ------------------------------------------------------------ serial executor
 def serial_execute(tasks, host, kernels):
     """Run tasks one by one in insertion order on copies of the host buffers.

@@ -35,6 +35,16 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops below (bench.py's single-thread vs
+ * all-core CPU baseline); results never depend on it. */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
 /* ---------------------------------------------------------------------
  * Vector addition ("performs the addition of two ... vectors").
  * c[i] = fl32(a[i] + b[i]): one IEEE-754 binary32 round-to-nearest add.

@@ -236,8 +236,9 @@ cudaError_t launch_tma(const float *img, int64_t H, int64_t W, const float *filt
 cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,
                        cudaStream_t st, int *launches) {
     if (H <= 0 || W <= 0) return cudaSuccess;
-    // TMA path: 16-byte aligned rows, int32 tile coordinates
-    if (radius == 2 && W % 4 == 0 && aligned16(img) && (W + 128) < (1ll << 31) &&
+    // TMA path: 16-byte aligned rows, 8-byte aligned output (its v2 stores),
+    // int32 tile coordinates
+    if (radius == 2 && W % 4 == 0 && aligned16(img) && ((uintptr_t)out & 7) == 0 && (W + 128) < (1ll << 31) &&
         (H + 64) < (1ll << 31) && ((W + 63) / 64) * ((H + 63) / 64) < (1ll << 31)) {
         bool done = false;
         cudaError_t e = launch_tma<2>(img, H, W, filt, out, st, &done);

@@ -896,8 +896,15 @@ int p2p_partner(const jacc_graph *g, int i) {
         return j;
     if (C.op == JACC_OP_ALLREDUCE_SUM && V.op == JACC_OP_REDUCE_SUM_F32 && C.args[0].buf == V.args[1].buf) return j;
     if (C.op == JACC_OP_ALLGATHER && V.op == JACC_OP_NBODY_STEP_F32 && C.args[0].buf == V.args[2].buf &&
-        V.args[1].count > 0)
-        return j;
+        V.args[1].count > 0) {
+        // The fused finish kernel publishes "ready" (peers may store into
+        // the gathered buffer) while its threads still read pos_src[tgt_offset
+        // + t].  Safe when the gathered buffer is not pos_src, or when the
+        // slots read are this rank's own slot of it (peers write only theirs).
+        const int64_t n_tgt = (int64_t)V.args[1].count;
+        const int64_t off = ((const jacc_nbody_params_t *)V.params.data())->tgt_offset;
+        if (C.args[1].buf != V.args[0].buf || off == (int64_t)g->cfg.rank * n_tgt) return j;
+    }
     return -1;
 }
 
@@ -1247,13 +1254,23 @@ int jacc_graph_add_task(jacc_graph_t *g, jacc_op_t op, const jacc_arg_t *args, i
     return JACC_OK;
 }
 
+// A failed execute may have run some kernels already: the device copies of
+// the buffers they wrote (e.g. a CACHABLE RW velocity in an N-body chain) no
+// longer equal the host values, which a failure leaves untouched (R8).  Drop
+// every residency claim so the next execute re-uploads from the host.
+static void drop_residency(jacc_graph *g) {
+    for (Buffer &B : g->bufs)
+        if (!B.device) B.dev_current = false;
+    g->planned = false;
+}
+
 int jacc_graph_execute(jacc_graph_t *g) {
     if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
     if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is already executing");
     ensure_plan(g);
     int rc = ensure_resources(g);
     if (rc == JACC_OK) rc = prepare_memory(g);
-    if (rc != JACC_OK) { g->state = ST_FAILED; return rc; }
+    if (rc != JACC_OK) { drop_residency(g); g->state = ST_FAILED; return rc; }
     ensure_plan(g);   // a device copy (re)allocated just now is not resident
     plan_counts(g, &g->stats);
     g->have_times = false;
@@ -1268,6 +1285,7 @@ int jacc_graph_execute(jacc_graph_t *g) {
     }
     if (rc != JACC_OK) {
         sync_all(g);   // drain what was issued; no D2H after the failure point
+        drop_residency(g);
         g->state = ST_FAILED;
         g->pending_error = rc;
         return rc;
@@ -1283,6 +1301,7 @@ int jacc_graph_sync(jacc_graph_t *g) {
     }
     int rc = sync_all(g);
     if (rc != JACC_OK) {
+        drop_residency(g);
         g->state = ST_FAILED;
         g->pending_error = rc;
         return rc;
@@ -1334,6 +1353,14 @@ int jacc_graph_task_ms(const jacc_graph_t *g, int task_id, float *ms) {
     if (g->cfg.flags & JACC_GRAPH_NO_TIMING) return fail(JACC_ERR_STATE, "graph created with JACC_GRAPH_NO_TIMING");
     if (!g->have_times) return fail(JACC_ERR_STATE, "no completed execute");
     *ms = g->tasks[task_id].ms;
+    return JACC_OK;
+}
+
+int jacc_graph_set_fail_task(jacc_graph_t *g, int32_t fail_task) {
+    if (!g || fail_task < 0) return fail(JACC_ERR_INVALID_ARG, "NULL graph or fail_task < 0");
+    if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is executing");
+    g->cfg.fail_task = fail_task;
+    g->planned = false;   // merge / fusion decisions depend on the hook
     return JACC_OK;
 }
 

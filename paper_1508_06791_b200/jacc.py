@@ -135,6 +135,7 @@ _lib.jacc_graph_execute.argtypes = [_vp]
 _lib.jacc_graph_sync.argtypes = [_vp]
 _lib.jacc_graph_stats.argtypes = [_vp, ctypes.POINTER(jacc_stats_t)]
 _lib.jacc_graph_task_ms.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+_lib.jacc_graph_set_fail_task.argtypes = [_vp, ctypes.c_int32]
 _lib.jacc_graph_dump.argtypes = [_vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
 _lib.jacc_buffer_invalidate.argtypes = [_vp, _vp]
 _lib.jacc_graph_destroy.argtypes = [_vp]
@@ -150,7 +151,8 @@ _lib.jacc_peer_alloc.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
 EXPORTS = ["jacc_graph_create", "jacc_graph_add_task", "jacc_graph_execute", "jacc_graph_sync",
            "jacc_graph_stats", "jacc_graph_task_ms", "jacc_graph_dump", "jacc_buffer_invalidate",
            "jacc_graph_destroy", "jacc_status_string", "jacc_last_error", "jacc_abi_version",
-           "jacc_abi_sizeof", "jacc_peer_init", "jacc_peer_connect", "jacc_peer_alloc"]
+           "jacc_abi_sizeof", "jacc_peer_init", "jacc_peer_connect", "jacc_peer_alloc",
+           "jacc_graph_set_fail_task"]
 
 jacc_graph_create = _lib.jacc_graph_create
 jacc_graph_add_task = _lib.jacc_graph_add_task
@@ -159,6 +161,7 @@ jacc_graph_sync = _lib.jacc_graph_sync
 jacc_graph_stats = _lib.jacc_graph_stats
 jacc_graph_task_ms = _lib.jacc_graph_task_ms
 jacc_graph_dump = _lib.jacc_graph_dump
+jacc_graph_set_fail_task = _lib.jacc_graph_set_fail_task
 jacc_buffer_invalidate = _lib.jacc_buffer_invalidate
 jacc_graph_destroy = _lib.jacc_graph_destroy
 jacc_status_string = _lib.jacc_status_string
@@ -193,7 +196,8 @@ def arg(ptr: int, count: int, dtype: int, access: int, flags: int = 0) -> jacc_a
 def _np_dtype(a: np.ndarray, f32x4: bool) -> tuple:
     if a.dtype == np.float32:
         if f32x4:
-            assert a.size % 4 == 0
+            if a.size % 4:
+                raise ValueError(f"f32x4 buffer of {a.size} floats is not a whole number of float4s")
             return JACC_F32X4, a.size // 4
         return JACC_F32, a.size
     if a.dtype == np.int32:
@@ -234,16 +238,23 @@ class Graph:
     def a(self, obj, access: int, cachable: bool = False, f32x4: bool = False) -> jacc_arg_t:
         flags = JACC_ARG_CACHABLE if cachable else 0
         if isinstance(obj, np.ndarray):
-            assert obj.flags.c_contiguous
+            if not obj.flags.c_contiguous:
+                raise ValueError("buffer must be C-contiguous")
             dt, n = _np_dtype(obj, f32x4)
             self._keep.append(obj)
             return arg(obj.ctypes.data, n, dt, access, flags)
         import torch  # torch tensors: device memory / pinned host memory
         if isinstance(obj, torch.Tensor):
-            assert obj.is_contiguous()
-            dt = {torch.float32: JACC_F32, torch.int32: JACC_I32}[obj.dtype]
+            if not obj.is_contiguous():
+                raise ValueError("tensor must be contiguous")
+            dts = {torch.float32: JACC_F32, torch.int32: JACC_I32}
+            if obj.dtype not in dts:
+                raise TypeError(f"unsupported dtype {obj.dtype}")
+            dt = dts[obj.dtype]
             n = obj.numel()
             if f32x4:
+                if obj.dtype != torch.float32 or n % 4:
+                    raise ValueError(f"f32x4 tensor of {n} {obj.dtype} is not a whole number of float4s")
                 dt, n = JACC_F32X4, n // 4
             if obj.is_cuda:
                 flags |= JACC_ARG_DEVICE
@@ -283,6 +294,10 @@ class Graph:
         ms = ctypes.c_float()
         check(jacc_graph_task_ms(self._h, task_id, ctypes.byref(ms)), "jacc_graph_task_ms")
         return ms.value
+
+    def set_fail_task(self, fail_task: int) -> None:
+        """Test hook (include/jacc.h jacc_graph_set_fail_task)."""
+        check(jacc_graph_set_fail_task(self._h, int(fail_task)), "jacc_graph_set_fail_task")
 
     def dump(self) -> str:
         need = ctypes.c_size_t()

@@ -161,3 +161,35 @@ def banded_csr(n: int = SPMV_N, nnz: int = SPMV_NNZ, bandwidth: int = 1600, seed
     row_ptr = np.cumsum(row_ptr, dtype=np.int64).astype(np.int32)
     val = (g.random(cols.size, dtype=np.float32) * 2 - 1).astype(np.float32)
     return row_ptr, cols, val
+
+
+def powerlaw_csr(n: int, mean_nnz: float = 8.0, seed: int = 1017, alpha: float = 1.6,
+                 empty_frac: float = 0.1, long_rows=(), ncols: int | None = None):
+    """Irregular CSR input: row lengths from a discrete power law (Pareto
+    tail with exponent `alpha`, scaled to about `mean_nnz` per row, capped
+    at ncols), a fraction `empty_frac` of rows empty, and explicit long rows
+    `long_rows = ((row, length), ...)`; columns uniform in [0, ncols), sorted
+    and unique within a row; values U[-1, 1).  (The irregular row-length mix
+    of a real sparse matrix such as bcsstk32, which is unavailable offline.)
+    Returns (row_ptr int32[n+1], col int32[nnz], val f32[nnz])."""
+    ncols = n if ncols is None else ncols
+    g = rng(seed)
+    lens = np.floor(g.pareto(alpha, n) * mean_nnz * (alpha - 1) / alpha * 1.5).astype(np.int64)
+    lens = np.minimum(lens, ncols)
+    lens[g.random(n) < empty_frac] = 0
+    for r, ln in long_rows:
+        lens[r] = min(ln, ncols)
+    cols = []
+    for r in np.nonzero(lens)[0]:
+        ln = int(lens[r])
+        if ln * 4 >= ncols:
+            c = np.sort(g.choice(ncols, ln, replace=False))
+        else:
+            c = np.unique(g.integers(0, ncols, ln + ln // 8 + 4))[:ln]
+            lens[r] = c.size
+        cols.append(c)
+    row_ptr = np.zeros(n + 1, np.int64)
+    row_ptr[1:] = np.cumsum(lens)
+    col = (np.concatenate(cols) if cols else np.zeros(0, np.int64)).astype(np.int32)
+    val = (g.random(col.size, dtype=np.float32) * 2 - 1).astype(np.float32)
+    return row_ptr.astype(np.int32), col, val

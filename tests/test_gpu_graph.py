@@ -163,11 +163,15 @@ def test_serializability_random_dags():
             _add(g, pool, t)
         g.run()
         for k, v in allbufs.items():
-            if v.dtype == np.int32:
-                assert np.array_equal(v, ref[k]), (k, tasks)
+            if k in ("s", "t"):
+                # reduction outputs: fp32 tree vs fp64 oracle (R14); a RW
+                # output also carries the accumulated host value
+                scale = np.maximum(np.abs(ref[k]), 1.0) * 5e-5
+                assert np.all(np.abs(v - ref[k]) <= scale), (k, tasks)
             else:
-                scale = np.maximum(np.abs(ref[k]), 1.0) * (5e-5 if k in "st" else 0)
-                assert np.all(np.abs(v - ref[k]) <= scale + 1e-6 * np.abs(ref[k])), (k, tasks)
+                # vadd / all-gather outputs (one RN fp32 add or a copy) and
+                # integer bins are exact by construction: "exactly"
+                assert np.array_equal(v, ref[k]), (k, tasks)
         g.destroy()
         done += 1
 
@@ -221,6 +225,47 @@ def test_failure_leaves_host_untouched():
     assert g.stats()["state"] == 3   # FAILED
     assert np.array_equal(c, c0) and np.array_equal(s, s0)
     g.destroy()
+
+
+@pytest.mark.parametrize("flags", [0, J.JACC_GRAPH_REPLAY])
+def test_failed_execute_drops_residency(flags):
+    """R8 + R5: a failed execute may already have run kernels that updated
+    the device copies of CACHABLE RW/W buffers (here the velocity and the
+    position ping-pong of an N-body chain); the host keeps the values of the
+    last successful execute, so the next execute must upload them again
+    instead of trusting the stale device copies."""
+    n, steps = 3000, 3
+    pos, vel = synth.nbody_state(n, seed=41)
+    vel[:, :3] = synth.rng(42).standard_normal((n, 3)).astype(np.float32) * 0.1
+    P = [pos.copy(), np.zeros_like(pos)]
+    V = vel.copy()
+    g = _graph(flags=flags)
+    prm = jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G)
+    for k in range(steps):
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(P[k % 2], R, True, f32x4=True), g.a(V, RW, True, f32x4=True),
+                                              g.a(P[(k + 1) % 2], W, True, f32x4=True)], prm)
+    g.run()                                   # execute 1: everything resident afterwards
+    host1 = [P[0].copy(), P[1].copy(), V.copy()]
+    g.set_fail_task(3)                        # execute 2: steps 0 and 1 run, step 2 fails
+    with pytest.raises(J.JaccError) as e:
+        g.run()
+    assert e.value.status == J.JACC_ERR_INJECTED
+    assert all(np.array_equal(x, y) for x, y in zip((P[0], P[1], V), host1))
+    g.set_fail_task(0)                        # execute 3 from the host state of execute 1
+    g.run()
+    st = g.stats()
+    assert st["h2d_count"] == 2, st           # P[0] and V re-uploaded, not taken as resident
+    g.destroy()
+    # reference: a fresh graph from execute 1's host state
+    P2 = [host1[0].copy(), host1[1].copy()]
+    V2 = host1[2].copy()
+    g = _graph()
+    for k in range(steps):
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(P2[k % 2], R, f32x4=True), g.a(V2, RW, f32x4=True),
+                                              g.a(P2[(k + 1) % 2], W, f32x4=True)], prm)
+    g.run()
+    g.destroy()
+    assert np.array_equal(V, V2) and np.array_equal(P[steps % 2], P2[steps % 2])
 
 
 def test_out_of_order_issue():

@@ -27,6 +27,26 @@ def _conv(img, f):
     return out
 
 
+def test_conv2d_misaligned_device_output():
+    """A caller-owned DEVICE output that is only 4-byte aligned (a view at an
+    odd element offset) must not reach the TMA kernel's 8-byte stores: it
+    takes the simple kernel, same results."""
+    import torch
+    h, w = 64, 256
+    img = synth.uniform_f32(h * w, 601, -1, 1).reshape(h, w)
+    f = synth.uniform_f32(25, 602, -1, 1).reshape(5, 5)
+    buf = torch.zeros(h * w + 1, device="cuda")
+    out = buf[1:].view(h, w)
+    assert out.data_ptr() % 8 == 4
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(torch.from_numpy(img).cuda(), R), g.a(torch.from_numpy(f).cuda(), R),
+                                      g.a(out, W)], jacc.jacc_conv2d_params_t(h, w, 2, 0))
+    g.run()
+    g.destroy()
+    ref, ab = oracle.conv2d(img, f)
+    assert np.all(np.abs(out.cpu().numpy().astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)
+
+
 # TMA path: W % 4 == 0 and r == 2 (ragged 64 x 64 tiles, tiny images, many
 # tiles per persistent block; 4739 x 4100 takes the 128 x 64 tile config,
 # >= 16 tiles per SM, with ragged tiles on both edges); the others take the
@@ -71,6 +91,42 @@ def test_spmv_tolerance(n, nnz, bw):
     g.destroy()
     ref, ab = oracle.spmv_csr(rp, col, val, x)
     assert np.all(np.abs(y - ref) <= 1e-5 * ab + 1e-30)
+
+
+def _spmv(rp, col, val, x, n):
+    y = np.full(n, np.nan, np.float32)     # W output: every row must be written
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_SPMV_CSR_F32, [g.a(rp, R), g.a(col, R), g.a(val, R), g.a(x, R), g.a(y, W)],
+               jacc.jacc_spmv_params_t(n, x.size))
+    g.run()
+    g.destroy()
+    return y
+
+
+# irregular rows (power-law lengths, ~1/3 empty, explicit long rows): the
+# lane kernel (30000 rows, one row of 12000) and the row-block stream kernel
+# (2^18 + 77 rows; the block holding a 6000-non-zero row exceeds the
+# 4096-product shared buffer and takes the per-row global path; a 30000 row)
+@pytest.mark.parametrize("n,mean,long_rows", [(30000, 12.0, ((17, 12000),)),
+                                              ((1 << 18) + 77, 8.0, ((1000, 6000), (200000, 30000),
+                                                                    ((1 << 18) + 76, 5000)))])
+def test_spmv_irregular_rows(n, mean, long_rows):
+    rp, col, val = synth.powerlaw_csr(n, mean, seed=n, long_rows=long_rows)
+    assert np.sum(np.diff(rp) == 0) > n // 10
+    x = synth.uniform_f32(n, 9, -1, 1)
+    y = _spmv(rp, col, val, x, n)
+    ref, ab = oracle.spmv_csr(rp, col, val, x)
+    assert np.all(np.abs(y.astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)
+    assert np.all(y[np.diff(rp) == 0] == 0.0)       # empty rows: exactly 0
+
+
+@pytest.mark.parametrize("n", [1, 1000, 1 << 18])
+def test_spmv_all_rows_empty(n):
+    rp = np.zeros(n + 1, np.int32)
+    col = np.zeros(0, np.int32); val = np.zeros(0, np.float32)
+    x = synth.uniform_f32(n, 10, -1, 1)
+    y = _spmv(rp, col, val, x, n)
+    assert np.all(y == 0.0)
 
 
 @pytest.mark.parametrize("shape", [(40, 50), (40, 132), (4739, 4100)])   # simple kernel / TMA path (zero-filled halo)

@@ -232,6 +232,78 @@ def test_p2p_world2_one_gpu(world):
             assert np.array_equal(ok["vel"], V1[lo:hi]), (r, flags)
 
 
+def _swap_worker(rank, world, port, q):
+    """N-body step whose targets are the OTHER rank's shard (tgt_offset !=
+    rank * n_tgt) with the all-gather's receive buffer = the step's pos_src:
+    the runtime must not fuse the all-gather into the finish kernel (peers
+    would overwrite slots it still reads); it runs standalone."""
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import synth
+        import paper_1508_06791_b200 as J
+        from paper_1508_06791_b200.torch_glue import make_graph, peer_setup, peer_tensor
+        n = 2048
+        pos, vel = synth.nbody_state(n, seed=34)
+        vel[:, :3] = synth.rng(35).standard_normal((n, 3)).astype(np.float32) * 0.1
+        res = {}
+        for swap in (True, False):
+            g, _ = make_graph(0, rank=rank, world=world, flags=J.JACC_GRAPH_P2P)
+            peer_setup(g, 8 << 20)
+            other = (rank + 1) % world if swap else rank
+            lo, hi = synth.shard_range(n, rank, world)
+            tlo, thi = synth.shard_range(n, other, world)
+            ALL = peer_tensor(g, (n, 4))
+            L0 = pinned(pos[lo:hi]); L1 = pinned(np.zeros((thi - tlo, 4), np.float32))
+            V = pinned(vel[tlo:thi])
+            prm = jacc.jacc_nbody_params_t(tlo, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G)
+            g.add_task(J.JACC_OP_ALLGATHER, [g.a(L0, R, f32x4=True), g.a(ALL, W, f32x4=True)])
+            g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(ALL, R, f32x4=True), g.a(V, RW, f32x4=True),
+                                                   g.a(L1, W, f32x4=True)], prm)
+            g.add_task(J.JACC_OP_ALLGATHER, [g.a(L1, R, f32x4=True), g.a(ALL, W, f32x4=True)])
+            g.run()
+            res[swap] = dict(all=ALL.cpu().numpy().copy(), vel=V.copy(), launches=g.stats()["launches"])
+            g.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+def test_p2p_nbody_gather_not_fused_when_unsafe():
+    import torch.multiprocessing as mp
+    world, n = 2, 2048
+    port = 29600 + (os.getpid() % 90)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_swap_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    pos, vel = synth.nbody_state(n, seed=34)
+    vel[:, :3] = synth.rng(35).standard_normal((n, 3)).astype(np.float32) * 0.1
+    P1, V1 = _single_gpu_nbody(pos, vel, 1)
+    sh = [synth.shard_range(n, r, world) for r in range(world)]
+    for r in range(world):
+        assert "error" not in out[r], out[r].get("error")
+        sw, al = out[r][True], out[r][False]
+        # swapped: slot q of ALL holds rank q's targets = shard (q + 1) % world
+        want = np.concatenate([P1[slice(*sh[(q + 1) % world])] for q in range(world)])
+        assert np.array_equal(sw["all"], want), r
+        assert np.array_equal(sw["vel"], V1[slice(*sh[(r + 1) % world])]), r
+        assert np.array_equal(al["all"], P1) and np.array_equal(al["vel"], V1[slice(*sh[r])]), r
+        # aligned: gather, partial, finish+gather (3); swapped: + a standalone gather (4)
+        assert (al["launches"], sw["launches"]) == (3, 4), (al["launches"], sw["launches"])
+
+
 def test_p2p_window_errors():
     """Error paths of the peer windows (include/jacc.h): a full window is
     JACC_ERR_OOM, handles whose window sizes differ are JACC_ERR_INVALID_ARG

@@ -53,6 +53,32 @@ def test_vadd_bit_exact(n):
     g.destroy()
 
 
+def test_vadd_ieee_specials_bit_exact():
+    """One IEEE RN fp32 add per element, specials included (the oracle is
+    pinned on them, tests/test_oracle_pins.py): +-Inf, NaN, -0, denormals
+    (no flush to zero), overflow to Inf, Inf - Inf = NaN, max-normal sums."""
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.17549435e-38,
+                   5.877472e-39, 3.4028235e38, -3.4028235e38, 1.0, -1.0, 2.0 ** -149 * 3,
+                   2.0 ** 24, 0.5], np.float32)
+    a = np.repeat(sp, sp.size)
+    b = np.tile(sp, sp.size)
+    # every pair, then a ragged tail that exercises the vector body and the
+    # scalar remainder with specials in every lane position
+    n = a.size * 257 + 3
+    a = np.resize(a, n); b = np.resize(np.roll(b, 5), n)
+    c = np.zeros(n, np.float32)
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(a, R), g.a(b, R), g.a(c, W)])
+    g.run()
+    g.destroy()
+    ref = oracle.vadd(a, b)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(c), nan)
+    assert np.array_equal(c[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+    assert np.any(c.view(np.uint32) == np.float32(-0.0).view(np.uint32))       # -0 + -0 = -0
+    assert np.any((c != 0) & (np.abs(c) < 1.17549435e-38))                      # denormal results kept
+
+
 @pytest.mark.parametrize("off", [1, 2, 3])
 def test_vadd_unaligned_device_args(off):
     n = 10007
@@ -313,25 +339,28 @@ def test_sgemm_gates(mode, shape):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("mode", [J.JACC_SGEMM_3XTF32], ids=["3xtf32"])
-def test_sgemm_full_size_config4_sampled(mode):
+@pytest.mark.parametrize("dist", ["unit", "signed"])
+def test_sgemm_full_size_config4_elementwise(dist):
+    """8192^3 (BASELINE config 4), EVERY element against the full fp64 oracle:
+    U[0,1) gate M1 (elementwise relative 1e-4); U[-1,1) gate M2 (normwise
+    1e-4 and componentwise 1e-4 (|A||B|)), plus Freivalds on the whole C."""
     n = synth.CFG4_MNK
-    for dist in ("unit", "signed"):
-        A, B = synth.sgemm_inputs(n, n, n, dist)
-        C = _sgemm(A, B, mode, device_args=True)
-        rows = np.concatenate([synth.rng(7).integers(0, n, 12), [0, n - 1]])
-        Ro = oracle.sgemm_rows(A, B, rows)
-        Cs = C[rows].astype(np.float64)
-        if dist == "unit":
-            assert np.max(np.abs(Cs - Ro) / np.abs(Ro)) <= 1e-4
-        else:
-            assert np.linalg.norm(Cs - Ro) <= 1e-4 * np.linalg.norm(Ro)
-        # Freivalds on the whole C (property at any size)
-        x = synth.rng(8).standard_normal(n)
-        lhs = C.astype(np.float64) @ x
-        rhs = A.astype(np.float64) @ (B.astype(np.float64) @ x)
-        bound = np.abs(A).astype(np.float64) @ (np.abs(B).astype(np.float64) @ np.abs(x))
-        assert np.all(np.abs(lhs - rhs) <= 1e-4 * bound)
+    A, B = synth.sgemm_inputs(n, n, n, dist)
+    C = _sgemm(A, B, J.JACC_SGEMM_3XTF32, device_args=True).astype(np.float64)
+    Ro = oracle.sgemm_rows(A, B)
+    if dist == "unit":
+        assert np.max(np.abs(C - Ro) / np.abs(Ro)) <= 1e-4
+    else:
+        assert np.linalg.norm(C - Ro) <= 1e-4 * np.linalg.norm(Ro)
+        # |A||B| is a GEMM of non-negative inputs: the oracle computes it too
+        AB = oracle.sgemm_rows(np.abs(A), np.abs(B))
+        assert np.all(np.abs(C - Ro) <= 1e-4 * AB)
+    del Ro
+    x = synth.rng(8).standard_normal(n)
+    lhs = C @ x
+    rhs = A.astype(np.float64) @ (B.astype(np.float64) @ x)
+    bound = np.abs(A).astype(np.float64) @ (np.abs(B).astype(np.float64) @ np.abs(x))
+    assert np.all(np.abs(lhs - rhs) <= 1e-4 * bound)
 
 
 # ----------------------------------------------------------------- N-body

@@ -166,3 +166,82 @@ def test_survey_count_table(name, tasks, naive, elided, second):
     resident = {a.buf for t in tasks for a in t.args if a.cachable and not a.device}
     c = counts(plan(tasks, resident=resident))
     assert (c["H2D"], c["D2H"]) == second
+
+
+# ------------------------------------------------ serial executor
+# serial_execute is the reference every GPU graph is compared with
+# (tests/test_gpu_graph.py serializability).  Pinned here against final
+# states derived BY HAND (literals below) on tiny integer-valued buffers, with
+# stand-in kernels written out in the test, so that a dropped auto-zero
+# (P:141), an RW accumulate that loses the host value, an
+# out-of-order execution or a mutated input fails one of them.
+import numpy as np  # noqa: E402
+
+from oracle.graph_model import serial_execute  # noqa: E402
+
+
+def _k_vadd(t, arr):
+    arr[2][...] = arr[0] + arr[1]
+
+
+def _k_reduce(t, arr):          # @Atomic(ADD) result += sum
+    arr[1][0] += arr[0].sum()
+
+
+def _k_hist(t, arr):            # bins[k] += #{key = k}
+    for k in arr[0]:
+        if 0 <= k < arr[1].size:
+            arr[1][k] += 1
+
+
+KS = {"vadd": _k_vadd, "reduce": _k_reduce, "hist": _k_hist}
+
+
+def test_serial_auto_zero_write_vs_readwrite():
+    keys = np.array([0, 2, 2, 3, 7, -1], np.int32)   # 7 and -1 out of range
+    host = {"k": keys, "bW": np.array([5, 5, 5, 5], np.int32),
+            "bRW": np.array([5, 5, 5, 5], np.int32)}
+    out = serial_execute([Task("hist", [Arg("k", READ), Arg("bW", WRITE)]),
+                          Task("hist", [Arg("k", READ), Arg("bRW", READWRITE)])], host, KS)
+    assert out["bW"].tolist() == [1, 0, 2, 1]        # W: auto-zeroed, then counted
+    assert out["bRW"].tolist() == [6, 5, 7, 6]       # RW: host value + counts
+    assert host["bW"].tolist() == [5, 5, 5, 5]       # the input state is not modified
+    s = {"x": np.array([1.0, 2.0, 4.0]), "s": np.array([100.0]), "t": np.array([100.0])}
+    out = serial_execute([Task("reduce", [Arg("x", READ), Arg("s", WRITE)]),
+                          Task("reduce", [Arg("x", READ), Arg("t", READWRITE)])], s, KS)
+    assert out["s"].tolist() == [7.0] and out["t"].tolist() == [107.0]
+
+
+def test_serial_raw_chain_and_insertion_order():
+    host = {"a": np.array([1.0, 2.0]), "b": np.array([10.0, 20.0]),
+            "c": np.array([0.0, 0.0]), "d": np.array([0.0, 0.0]), "s": np.array([0.0])}
+    # t0: c = a + b; t1: d = c + b (RAW on c); t2: s = sum(d) (RAW on d);
+    # t3: c = a + a (WAR after t1 read c, WAW after t0) -- t1 must have seen
+    # t0's c, not t3's.
+    tasks = [Task("vadd", [Arg("a", READ), Arg("b", READ), Arg("c", WRITE)]),
+             Task("vadd", [Arg("c", READ), Arg("b", READ), Arg("d", WRITE)]),
+             Task("reduce", [Arg("d", READ), Arg("s", WRITE)]),
+             Task("vadd", [Arg("a", READ), Arg("a", READ), Arg("c", WRITE)])]
+    out = serial_execute(tasks, host, KS)
+    assert out["d"].tolist() == [21.0, 42.0]
+    assert out["s"].tolist() == [63.0]
+    assert out["c"].tolist() == [2.0, 4.0]
+    # reversed WAR pair: now t1 reads the LATER c
+    out2 = serial_execute([tasks[0], tasks[3], tasks[1]], host, KS)
+    assert out2["d"].tolist() == [12.0, 24.0]
+
+
+def test_serial_read_read_independent_and_accumulate_order():
+    host = {"x": np.array([3.0, 4.0]), "s": np.array([1.0]), "t": np.array([0.0])}
+    # two readers of x in either order give the same result (no edge, R9)
+    t_s = Task("reduce", [Arg("x", READ), Arg("s", READWRITE)])
+    t_t = Task("reduce", [Arg("x", READ), Arg("t", WRITE)])
+    for order in ([t_s, t_t], [t_t, t_s]):
+        out = serial_execute(order, host, KS)
+        assert out["s"].tolist() == [8.0] and out["t"].tolist() == [7.0]
+        assert out["x"].tolist() == [3.0, 4.0]
+    # RW accumulates across tasks (1 + 7 + 7); a W in between restarts at 0
+    out = serial_execute([t_s, t_s], host, KS)
+    assert out["s"].tolist() == [15.0]
+    out = serial_execute([t_s, Task("reduce", [Arg("x", READ), Arg("s", WRITE)]), t_s], host, KS)
+    assert out["s"].tolist() == [14.0]
