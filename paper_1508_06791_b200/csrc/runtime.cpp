@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1264,12 +1266,28 @@ static void drop_residency(jacc_graph *g) {
     g->planned = false;
 }
 
+// JACC_LOG=1: host-side phase times of every execute on stderr (issue
+// latency diagnostics; nothing is logged otherwise).
+static bool log_on() {
+    static const bool on = [] { const char *e = getenv("JACC_LOG"); return e && e[0] == '1'; }();
+    return on;
+}
+static double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int jacc_graph_execute(jacc_graph_t *g) {
     if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
     if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is already executing");
+    const double t0 = log_on() ? now_us() : 0.0;
     ensure_plan(g);
+    const double t1 = log_on() ? now_us() : 0.0;
     int rc = ensure_resources(g);
+    const double t2 = log_on() ? now_us() : 0.0;
     if (rc == JACC_OK) rc = prepare_memory(g);
+    if (log_on())
+        fprintf(stderr, "[jacc] execute: plan %.1f us, resources %.1f us, memory %.1f us\n", t1 - t0, t2 - t1,
+                now_us() - t2);
     if (rc != JACC_OK) { drop_residency(g); g->state = ST_FAILED; return rc; }
     ensure_plan(g);   // a device copy (re)allocated just now is not resident
     plan_counts(g, &g->stats);
@@ -1281,7 +1299,9 @@ int jacc_graph_execute(jacc_graph_t *g) {
         rc = issue_replay(g);
         g->last_was_replay = rc == JACC_OK && g->stats.graph_replays + g->stats.graph_captures > before;
     } else {
+        const double t3 = log_on() ? now_us() : 0.0;
         rc = issue(g);
+        if (log_on()) fprintf(stderr, "[jacc] execute: issue %.1f us (%zu actions)\n", now_us() - t3, g->plan.size());
     }
     if (rc != JACC_OK) {
         sync_all(g);   // drain what was issued; no D2H after the failure point

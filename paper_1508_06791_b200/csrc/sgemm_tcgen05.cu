@@ -10,11 +10,15 @@
 // tolerance (1e-4 vs the fp64 oracle; DESIGN.md §SGEMM shows 1xTF32 does not
 // on signed inputs).
 //
-// Kernels:
-//   1. split_a: A (M x K, lda) -> A_hi, A_lo  [Mp x Kp], K-major, zero padded;
-//   2. split_bt: B (K x N, ldb) -> B_hi^T, B_lo^T [Np x Kp] (transposed through
-//      shared memory so both UMMA operands are K-major), zero padded;
-//   3. gemm: one 128 x 256 output tile per CTA, warp-specialised --
+// Two paths, the same three MMAs in the same order (bitwise-equal results,
+// tested):
+//   * default (16-byte aligned A, B and row strides): gemm_3xtf32_pair_kernel
+//     -- a CTA pair per 256 x 256 tile (tcgen05 cta_group::2), raw A and B
+//     tiles by TMA (B row-major = MN-major operand, no transpose), the hi
+//     operand is the raw tile (the tensor core reads only the TF32 bits),
+//     x_lo computed in shared memory by the epilogue warps; no pre-pass;
+//   * fallback: split_a / split_bt write padded K-major hi/lo copies, then
+//     gemm_3xtf32_kernel -- one 128 x 256 tile per CTA:
 //        warp 0     TMA producer: per 16-wide K block, 4 boxes (A_hi, A_lo:
 //                   128x16; B_hi, B_lo: 256x16) into a 4-stage mbarrier ring
 //                   (48 KB per stage), 64B-swizzled;
@@ -27,10 +31,13 @@
 //                   registers, fp32 round-to-nearest accumulation of the
 //                   chunk sums (see the kernel comment), then global stores
 //                   (edge-guarded).
+// Measured at 8192^3 (one B200, events): pre-split path 3.87 ms (split
+// 0.25 ms + GEMM; 6.4 GB DRAM per task), pair path 3.50 ms (2.55 GB).
 // Every output element accumulates its K products in the same order for any
 // M/N blocking, so a row block of C computed on one rank equals the same rows
 // computed on one GPU bit for bit.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -305,6 +312,276 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------------------ in-kernel split, CTA pair (v2)
+// The same 3xTF32 product without the split pre-pass, on 256 x 256 output
+// tiles computed by a CTA PAIR (a (2,1,1) cluster, tcgen05 cta_group::2).
+//
+// * The raw fp32 tiles of A (K-major, as stored) and B (row-major K x N =
+//   MN-major for the B operand: no transpose) arrive by TMA.  The tensor
+//   core's kind::tf32 operand read takes only the TF32 bits of an fp32 word
+//   (hw(x) = x & 0xFFFFE000 = x_hi -- pinned bitwise against the pre-split
+//   path by tests/test_gpu_parity.py), so the raw tile IS the hi operand.
+// * The epilogue warps, idle between chunk drains, write x_lo = x - x_hi of
+//   every staged element next to it (same swizzled position: the split is
+//   elementwise), then signal the leader CTA:
+//       A.B ~= A.B(hw) + A.B_lo + A_lo.B
+// * Pair: CTA r holds A rows [128 r, 128 r + 128) and B columns
+//   [128 r, 128 r + 128) of the tile; the leader's single thread issues
+//   tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8), which reads both
+//   CTAs' shared memory and writes rows [128 r, ...) of D into CTA r's TMEM.
+//   Per SM and K block the tensor core reads 8 KB per MMA instead of 12 KB
+//   (1-SM 128 x 256), which leaves shared-memory bandwidth for the split:
+//   measured with 1-SM tiles, TMA writes + split + MMA reads (~187 B/clk)
+//   oversubscribed the ~128 B/clk of shared memory (4.07 ms at 8192^3 vs
+//   3.28 ms without the split); the pair needs ~125 B/clk.
+// DRAM traffic: A and B once per tile (plus L2 misses), no hi/lo copies.
+// Stage (K = 16) per CTA: A 8 KB + A_lo 8 KB (SW64 K-major) + B 8 KB + B_lo
+// 8 KB (four 16 x 32 boxes, 128B swizzle with 32B atoms, MN-major).
+constexpr int kPairBM = 2 * BM;                      // 256 rows per pair
+constexpr int kHalfBN = BN / 2;                      // 128 B columns per CTA
+constexpr int kBBox = 32;                            // B columns per TMA box (128 B rows)
+constexpr int kBBoxBytes = BK * kBBox * 4;           // 2 KB
+constexpr int kHBBytes = kHalfBN * BK * 4;           // 8 KB
+constexpr int kStage2 = 2 * kABytes + 2 * kHBBytes;  // 32 KB
+constexpr int kStages2 = 6;
+constexpr int kSmem2 = kStages2 * kStage2 + 1024 + 256;
+// kind::tf32, D f32, A K-major, B MN-major, M = 256, N = 256
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(kPairBM >> 4) << 24);
+
+// MN-major tf32 operands exist only in the 128-byte swizzle with 32-byte
+// atoms (UMMA layout type SWIZZLE_128B_BASE32B = 1; TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 32 fp32 along N per 128-byte row, the
+// pattern repeating every 4 K rows (512 B).  (The plain 128B swizzle is
+// accepted by the instruction and silently yields zeros -- measured.)
+__device__ __forceinline__ uint64_t desc_b_mn(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFF) >> 4);              // start address
+    d |= (uint64_t)(kBBoxBytes >> 4) << 16;              // LBO: next 32-column (MN) group = next box
+    d |= (uint64_t)(512 >> 4) << 32;                     // SBO: next 4-row (K) swizzle atom
+    d |= (uint64_t)1 << 46;                              // version 1
+    d |= (uint64_t)1 << 61;                              // SWIZZLE_128B_BASE32B
+    return d;
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc2), "r"(accum));
+}
+// arrive on the mbarriers at this address in BOTH CTAs of the pair once the
+// leader's MMAs issued so far have completed
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// arrive on the leader CTA's (rank 0) mbarrier at the same offset.  The
+// default (.release, .cta scope) form: an explicit .release.cluster arrive
+// compiles to MEMBAR.ALL.GPU + ERRBAR per arrive, which measured 40 % of the
+// split warps' stall samples and made the pair kernel 2x slower.
+__device__ __forceinline__ void arrive_leader(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                            float *__restrict__ C, int64_t M, int64_t N, int64_t ldc, int num_kb, int num_m2,
+                            int num_n, float *__restrict__ part, int64_t Mp, int64_t Np) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *bars = (uint64_t *)(smem + kStages2 * kStage2);
+    uint32_t *tmem_slot = (uint32_t *)(bars + 3 * kStages2 + 4);
+    // full: this CTA's TMA landed its raw tiles; empty: the pair's MMAs read
+    // the stage (multicast commit); split: both CTAs wrote their lo tiles
+    // (leader's, 16 arrivals); tfull / tempty: accumulator buffer handshake
+    // (tempty: leader's, 16 arrivals)
+    const uint32_t full_bar0 = smem_u32(bars), empty_bar0 = smem_u32(bars + kStages2),
+                   split_bar0 = smem_u32(bars + 2 * kStages2), tfull0 = smem_u32(bars + 3 * kStages2),
+                   tempty0 = smem_u32(bars + 3 * kStages2 + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    constexpr int kGroupM = 8;                       // pair tiles (256 rows) per raster group
+    const int pid = blockIdx.x >> 1;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m2 - first_m, kGroupM);
+    const int m_blk = first_m + (pid % per_group) % gm;
+    const int n_blk = (pid % per_group) / gm;
+    const int all_chunks = (num_kb + kChunkKB - 1) / kChunkKB;
+    const int per_split = (all_chunks + gridDim.y - 1) / gridDim.y;
+    const int c_begin = blockIdx.y * per_split, c_end = min(all_chunks, c_begin + per_split);
+    const int kb_begin = c_begin * kChunkKB, kb_end = min(num_kb, c_end * kChunkKB);
+    const int nchunks = c_end > c_begin ? c_end - c_begin : 0;
+    const int nkb = kb_end > kb_begin ? kb_end - kb_begin : 0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&map_a); tma_prefetch(&map_b);
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(full_bar0 + 8 * s, 1);
+            mbar_init(empty_bar0 + 8 * s, 1);
+            mbar_init(split_bar0 + 8 * s, 2 * kEpiWarps);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, 2 * kEpiWarps);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) {   // both CTAs' warp 1: one 2-SM allocation at the same TMEM address
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();    // barriers initialised in both CTAs before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- TMA producer (each CTA): its A rows and its B columns
+            for (int i = 0; i < nkb; ++i) {
+                const int kb = kb_begin + i, s = i % kStages2;
+                mbar_wait(empty_bar0 + 8 * s, ((i / kStages2) & 1) ^ 1);
+                uint8_t *st = smem + s * kStage2;
+                const uint32_t fb = full_bar0 + 8 * s;
+                mbar_expect_tx(fb, kABytes + kHBBytes);
+                tma_load_2d(smem_u32(st), &map_a, kb * BK, m_blk * kPairBM + (int)rank * BM, fb);
+                const uint32_t bdst = smem_u32(st + 2 * kABytes);
+#pragma unroll
+                for (int j = 0; j < kHalfBN / kBBox; ++j)
+                    tma_load_2d(bdst + j * kBBoxBytes, &map_b, n_blk * BN + (int)rank * kHalfBN + j * kBBox,
+                                kb * BK, fb);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {   // ---- MMA issuer: the leader's single thread
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % kStages2;
+                const int chunk = i / kChunkKB, buf = chunk & 1;
+                const bool first = (i % kChunkKB) == 0;
+                const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
+                const uint32_t tmem_d = tmem_base + buf * BN;
+                if (first) {
+                    mbar_wait(tempty0 + 8 * buf, ((chunk >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                mbar_wait(split_bar0 + 8 * s, (i / kStages2) & 1);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * kStage2);
+                const uint32_t a_raw = base, a_lo = base + kABytes, b_raw = base + 2 * kABytes,
+                               b_lo = base + 2 * kABytes + kHBBytes;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t oa = k * 32, ob = k * 1024;   // A: 32 B along K; B: 8 rows of 128 B
+                    mma_tf32_pair(tmem_d, smem_desc(a_raw + oa), desc_b_mn(b_raw + ob), !(first && k == 0));
+                    mma_tf32_pair(tmem_d, smem_desc(a_raw + oa), desc_b_mn(b_lo + ob), 1);
+                    mma_tf32_pair(tmem_d, smem_desc(a_lo + oa), desc_b_mn(b_raw + ob), 1);
+                }
+                commit_pair(empty_bar0 + 8 * s);
+                if (last) commit_pair(tfull0 + 8 * buf);
+            }
+        }
+    } else {   // ---- warps 2..9 (each CTA): split the staged tiles, drain the chunk sums
+        const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+        float acc[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+        int drained = 0;
+        auto drain = [&](int chunk) {
+            const int buf = chunk & 1;
+            mbar_wait(tfull0 + 8 * buf, (chunk >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + h * 128;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t r[32];
+                TMEM_LD_32(taddr + j * 32, r);
+                tc::wait_ld();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) acc[j * 32 + t] += __uint_as_float(r[t]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(tempty0 + 8 * buf);
+        };
+        constexpr int kVec = (kABytes + kHBBytes) / 16;         // float4s to split per stage
+        constexpr int kPer = kVec / (kEpiWarps * 32);           // 4 per thread
+        const int et = ew * 32 + lane;
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % kStages2;
+            mbar_wait(full_bar0 + 8 * s, (i / kStages2) & 1);
+            uint8_t *st = smem + s * kStage2;
+            float4 v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int f = et + u * kEpiWarps * 32;           // float4 index over [A | B]
+                const int off = f < kABytes / 16 ? f * 16 : 2 * kABytes + (f * 16 - kABytes);
+                v[u] = *(const float4 *)(st + off);
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int f = et + u * kEpiWarps * 32;
+                const int off = f < kABytes / 16 ? f * 16 + kABytes : 2 * kABytes + kHBBytes + (f * 16 - kABytes);
+                float4 l;
+                l.x = v[u].x - tf32_hi(v[u].x); l.y = v[u].y - tf32_hi(v[u].y);
+                l.z = v[u].z - tf32_hi(v[u].z); l.w = v[u].w - tf32_hi(v[u].w);
+                *(float4 *)(st + off) = l;
+            }
+            // generic-proxy stores -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) arrive_leader(split_bar0 + 8 * s);
+            // chunk c's MMAs need nothing more from this CTA once chunk c+1
+            // is split: drain it now (the leader still has the staged stages
+            // of chunk c+1 to issue)
+            if ((i % kChunkKB) == kChunkKB - 1 && i / kChunkKB >= 1) drain(drained++);
+        }
+        while (drained < nchunks) drain(drained++);
+        const int64_t row = (int64_t)m_blk * kPairBM + (int64_t)rank * BM + q * 32 + lane;
+        if (part) {
+            float *prow = part + ((int64_t)blockIdx.y * Mp + row) * Np + (int64_t)n_blk * BN + h * 128;
+#pragma unroll
+            for (int j = 0; j < 128; j += 4)
+                *(float4 *)(prow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else if (row < M) {
+            float *crow = C + row * ldc;
+            const int64_t col0 = (int64_t)n_blk * BN + h * 128;
+            if (col0 + 128 <= N && ((ldc & 3) == 0) && (((uintptr_t)C & 15) == 0)) {
+#pragma unroll
+                for (int j = 0; j < 128; j += 4)
+                    *(float4 *)(crow + col0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    if (col0 + j < N) crow[col0 + j] = acc[j];
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();    // the leader's MMAs read both CTAs' smem: nobody leaves early
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+    }
+}
+
 // C = sum of the split partials, in split order.  One row per blockIdx.y,
 // four columns per thread (16-byte partial loads; Np is a multiple of 256).
 __global__ void __launch_bounds__(256) split_sum_f32_kernel(const float *__restrict__ part, int splits, int64_t Mp,
@@ -346,13 +623,25 @@ bool make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t kp, int b
     return tc::make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, kp, kp * 4, box_rows, BK, kSw);
 }
 
+// JACC_SGEMM_V1=1: force the split pre-pass path (A/B comparisons only)
+bool getenv_flag_v1() {
+    static const bool v = [] { const char *e = getenv("JACC_SGEMM_V1"); return e && e[0] == '1'; }();
+    return v;
+}
+
 }  // namespace
 
 size_t sgemm_3xtf32_ws_bytes(const jacc_sgemm_params_t *p) {
     const int64_t Mp = round_up(p->M > 0 ? p->M : 1, BM), Np = round_up(p->N > 0 ? p->N : 1, BN),
                   Kp = round_up(p->K > 0 ? p->K : 1, BK);
     const int splits = sgemm_splits((Mp / BM) * (Np / BN), Kp);
-    return (size_t)(2 * Mp * Kp + 2 * Np * Kp) * 4 + 4096 + (splits > 1 ? (size_t)splits * Mp * Np * 4 + 1024 : 0);
+    const size_t v1 = (size_t)(2 * Mp * Kp + 2 * Np * Kp) * 4 + 4096 + (splits > 1 ? (size_t)splits * Mp * Np * 4 + 1024 : 0);
+    // the pair path needs only its split-K partials (alignment decides the
+    // path at launch, so provide for both)
+    const int64_t Mp2 = round_up(p->M > 0 ? p->M : 1, kPairBM);
+    const int splits2 = sgemm_splits(2 * (Mp2 / kPairBM) * (Np / BN), Kp);
+    const size_t v2 = splits2 > 1 ? (size_t)splits2 * Mp2 * Np * 4 + 1024 : 0;
+    return v1 > v2 ? v1 : v2;
 }
 
 cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sgemm_params_t *p, void *ws,
@@ -362,6 +651,32 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
     if (K == 0)   // C = 0 (beta = 0): the M x N window only
         return cudaMemset2DAsync(C, (size_t)p->ldc * 4, 0, (size_t)N * 4, (size_t)M, st);
     const int64_t Mp = round_up(M, BM), Np = round_up(N, BN), Kp = round_up(K, BK);
+    const int num_m = (int)(Mp / BM), num_n = (int)(Np / BN);
+    const int splits = sgemm_splits((int64_t)num_m * num_n, Kp);
+    // v2 (CTA pair, in-kernel split, no pre-pass): TMA straight from A and
+    // B, which needs 16-byte aligned bases and row strides
+    if (aligned16(A) && aligned16(B) && (p->lda & 3) == 0 && (p->ldb & 3) == 0 && !getenv_flag_v1()) {
+        CUtensorMap m_a, m_b;
+        if (tc::make_map_2d(&m_a, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, K, p->lda * 4, BM, BK, kSw) &&
+            tc::make_map_2d_swz(&m_b, B, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, K, N, p->ldb * 4, BK, kBBox,
+                                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+            cudaError_t e = set_max_dyn_smem((const void *)gemm_3xtf32_pair_kernel, kSmem2);
+            if (e != cudaSuccess) return e;
+            const int64_t Mp2 = round_up(M, kPairBM);
+            const int num_m2 = (int)(Mp2 / kPairBM);
+            const int splits2 = sgemm_splits(2 * (int64_t)num_m2 * num_n, Kp);
+            float *part = splits2 > 1 ? (float *)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023) : nullptr;
+            gemm_3xtf32_pair_kernel<<<dim3(2 * num_m2 * num_n, splits2), kThreads, kSmem2, st>>>(
+                m_a, m_b, C, M, N, p->ldc, (int)(Kp / BK), num_m2, num_n, part, Mp2, Np);
+            ++*launches;
+            if (part) {
+                split_sum_f32_kernel<<<dim3((unsigned)((N + 1023) / 1024), (unsigned)M), 256, 0, st>>>(
+                    part, splits2, Mp2, Np, C, M, N, p->ldc);
+                ++*launches;
+            }
+            return cudaGetLastError();
+        }
+    }
     float *ahi = (float *)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
     float *alo = ahi + Mp * Kp;
     float *bhi = alo + Mp * Kp;
@@ -379,8 +694,6 @@ cudaError_t sgemm_3xtf32(const float *A, const float *B, float *C, const jacc_sg
         return cudaErrorInvalidValue;
     cudaError_t e = set_max_dyn_smem((const void *)gemm_3xtf32_kernel, kSmemBytes);
     if (e != cudaSuccess) return e;
-    const int num_m = (int)(Mp / BM), num_n = (int)(Np / BN);
-    const int splits = sgemm_splits((int64_t)num_m * num_n, Kp);
     float *part = splits > 1 ? (float *)(((uintptr_t)(blo + Np * Kp) + 1023) & ~(uintptr_t)1023) : nullptr;
     gemm_3xtf32_kernel<<<dim3(num_m * num_n, splits), kThreads, kSmemBytes, st>>>(
         m_ahi, m_alo, m_bhi, m_blo, C, M, N, p->ldc, (int)(Kp / BK), num_m, num_n, part, Mp, Np);

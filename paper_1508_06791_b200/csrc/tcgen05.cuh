@@ -103,19 +103,23 @@ inline encode_fn_t get_encode() {
 // (row stride `ld_bytes`), box [box_rows x box_cols], swizzle `sw` bytes
 // (0 = none: the box lands row-major, box_cols contiguous).  Out-of-bounds
 // box elements (negative or past-the-end coordinates) are filled with zeros.
-inline bool make_map_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize, int64_t rows,
-                        int64_t cols, int64_t ld_bytes, int box_rows, int box_cols, int sw) {
+inline bool make_map_2d_swz(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
+                            int64_t ld_bytes, int box_rows, int box_cols, CUtensorMapSwizzle swz) {
     encode_fn_t enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld_bytes};
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
+    return enc(m, dt, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+inline bool make_map_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize, int64_t rows,
+                        int64_t cols, int64_t ld_bytes, int box_rows, int box_cols, int sw) {
     (void)esize;
-    return enc(m, dt, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               sw == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return make_map_2d_swz(m, base, dt, rows, cols, ld_bytes, box_rows, box_cols,
+                           sw == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                          : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace tc

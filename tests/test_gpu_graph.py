@@ -282,6 +282,11 @@ def test_out_of_order_issue():
     g.add_task(J.JACC_OP_VADD_F32, [g.a(x, R), g.a(y, R), g.a(z, W)])
     streams = [int(l.split("stream=")[1].split()[0]) for l in g.dump().splitlines() if l.startswith("task")]
     assert streams[0] != streams[1]
+    # warm-up execute: the first one allocates the device copies (torch's
+    # caching allocator may cudaMalloc) and loads the kernels' module (lazy
+    # loading), both of which can block the host thread for the length of
+    # the copies; the second execute re-copies a and b (not CACHABLE)
+    g.run()
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_start.record(st["h2d"])

@@ -510,3 +510,48 @@ def test_nbody_shard_invariance_bitwise():
                                                g.a(p, W, f32x4=True)], jacc.jacc_nbody_params_t(lo, 0.016, 0.01, 1.0))
         g.run(); g.destroy()
         assert np.array_equal(v, full_v[lo:hi]) and np.array_equal(p, full_p[lo:hi])
+
+
+_V1_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import synth, torch
+import paper_1508_06791_b200 as J
+from paper_1508_06791_b200 import jacc
+from paper_1508_06791_b200.torch_glue import make_graph
+M, N, K, seed = map(int, sys.argv[2:6])
+A, B = synth.sgemm_inputs(M, N, K, "signed", seed=seed)
+C = np.zeros((M, N), np.float32)
+g, _ = make_graph(0)
+g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A, 1), g.a(B, 1), g.a(C, 2)],
+           jacc.jacc_sgemm_params_t(M, N, K, K, N, N, J.JACC_SGEMM_3XTF32, 0))
+g.run(); g.destroy()
+np.save(sys.argv[6], C)
+"""
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 256), (300, 520, 1000), (1000, 1000, 4096), (2048, 2048, 1024)])
+def test_sgemm_inkernel_split_bitwise_equals_presplit(shape, tmp_path):
+    """The default path feeds the RAW fp32 tiles to kind::tf32 as the hi
+    operand (the tensor core reads only the TF32 bits) and splits lo inside
+    the kernel; the pre-split path (JACC_SGEMM_V1=1) writes x_hi = x &
+    0xFFFFE000 and x_lo = x - x_hi to memory first.  Both issue the same
+    three MMAs in the same order, so they agree BIT FOR BIT exactly when the
+    hardware's operand read is that truncation -- which this pins."""
+    import os
+    import subprocess
+    import sys
+    M, N, K = shape
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for v1 in ("0", "1"):
+        f = str(tmp_path / f"c{v1}.npy")
+        env = dict(os.environ, JACC_SGEMM_V1=v1)
+        r = subprocess.run([sys.executable, "-c", _V1_SCRIPT, root, str(M), str(N), str(K), "77", f],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[v1] = np.load(f)
+    assert np.array_equal(outs["0"].view(np.uint32), outs["1"].view(np.uint32))
+    A, B = synth.sgemm_inputs(M, N, K, "signed", seed=77)
+    Ro = oracle.sgemm_rows(A, B)
+    assert np.linalg.norm(outs["0"] - Ro) <= 1e-4 * np.linalg.norm(Ro)
