@@ -39,6 +39,7 @@ WORKLOAD = ("jacc-suite: cfg1 vadd+reduce 2^20 f32, cfg2 histogram 2^28 i32 -> 2
             "2^26 f32, cfg4 SGEMM 8192^3 f32 (3xTF32 tcgen05), cfg5 N-body 2^17 bodies x 10 steps; one "
             "task graph per step")
 NBODY_FLOP = 20   # conventional flops per body-body interaction
+L2_BYTES = 126 << 20   # B200 L2
 
 
 def _peaks():
@@ -304,6 +305,13 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
         if name not in units or not ts:
             continue
         ms = statistics.mean(ts)
+        if name in ("vadd", "reduce", "hist", "bs") and units[name] < L2_BYTES // 2:
+            # cfg1's 2^20 working set (12.6 MB) is L2-resident and shorter than
+            # the launch ramp: a latency, not an HBM-roofline point (the
+            # paper-size and 2^28 points are in roofline_points)
+            out[name] = {"bound": "latency (L2-resident)", "ms": ms, "us": ms * 1e3, "launches": len(ts),
+                         "bytes_per_launch": units[name]}
+            continue
         if name in ("vadd", "reduce", "hist", "bs"):
             ach = units[name] / (ms * 1e-3) / 1e9
             out[name] = {"bound": "hbm", "ms": ms, "achieved": ach, "unit": "GB/s", "peak": hbm, "frac": ach / hbm,
@@ -458,35 +466,115 @@ def cpu_baseline_leg():
 
 # ------------------------------------------------------------ main arm
 def roofline_points(torch, J, peaks, reps=10):
-    """The HBM kernels of config 1 at a size where HBM, not launch latency or
-    L2, binds (2^28 elements, SURVEY §8(d) "roofline points"), L2 flushed
-    before every launch; device time from the task's CUDA events."""
+    """The HBM kernels of config 1 at the paper's sizes (vadd 2^24, P:476-477;
+    reduce 2^25) and at 2^28 (SURVEY §8(d) roofline points).  Two
+    timings per point:
+      * isolated: L2 flushed (write + read) before every launch, device time
+        of the one launch from its task's CUDA events (includes the launch
+        ramp and the event pair);
+      * back_to_back: R launches on R DISTINCT buffers (so every launch reads
+        cold data: R x the working set >> L2) replayed as one CUDA graph, one
+        event pair around all R on the launching stream; per-launch time =
+        total / R (the event overhead amortised; inter-launch gaps included).
+    `achieved`/`frac` use the back-to-back per-launch time."""
     from paper_1508_06791_b200.torch_glue import make_graph
-    R, W = J.JACC_READ, J.JACC_WRITE
-    n = 1 << 28
+    R_, W_ = J.JACC_READ, J.JACC_WRITE
     dev = torch.device("cuda", torch.cuda.current_device())
-    a = torch.rand(n, device=dev); b = torch.rand(n, device=dev)
-    c = torch.empty(n, device=dev); s = torch.zeros(1, device=dev)
     flush = L2Flush(torch, dev)
     out = {}
-    for name, op, args, nbytes in (("vadd", J.JACC_OP_VADD_F32, lambda g: [g.a(a, R), g.a(b, R), g.a(c, W)], 12 * n),
-                                   ("reduce", J.JACC_OP_REDUCE_SUM_F32, lambda g: [g.a(a, R), g.a(s, W)], 4 * n)):
+    for name, n, copies in (("vadd_2p24", 1 << 24, 8), ("reduce_2p25", 1 << 25, 8),
+                            ("vadd_2p28", 1 << 28, 2), ("reduce_2p28", 1 << 28, 2)):
+        is_vadd = name.startswith("vadd")
+        nbytes = (12 if is_vadd else 4) * n
+        bufs = []
+        for _ in range(copies):
+            if is_vadd:
+                bufs.append((torch.rand(n, device=dev), torch.rand(n, device=dev), torch.empty(n, device=dev)))
+            else:
+                bufs.append((torch.rand(n, device=dev), torch.zeros(1, device=dev)))
+
+        def add(g, b):
+            if is_vadd:
+                g.add_task(J.JACC_OP_VADD_F32, [g.a(b[0], R_), g.a(b[1], R_), g.a(b[2], W_)])
+            else:
+                g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(b[0], R_), g.a(b[1], W_)])
+        # isolated launches
         g, _ = make_graph(dev.index, n_streams=1)
-        g.add_task(op, args(g))
-        ms = []
+        add(g, bufs[0])
+        iso = []
         for i in range(reps + 2):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             g.run()
             if i >= 2:
+                iso.append(g.task_ms(0))
+        g.destroy()
+        # back to back over distinct buffers, one replayed graph
+        g, st = make_graph(dev.index, n_streams=1,
+                           flags=J.JACC_GRAPH_SERIAL | J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING)
+        for b in bufs:
+            add(g, b)
+        g.run()   # capture
+        comp = st["compute"][0]
+        b2b = []
+        for i in range(max(3, reps // 2)):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(comp)
+            g.execute()
+            e1.record(comp)
+            g.sync()
+            torch.cuda.synchronize()
+            b2b.append(e0.elapsed_time(e1) / copies)
+        g.destroy()
+        m_iso, m_b2b = statistics.mean(iso), statistics.median(b2b)
+        ach = nbytes / (m_b2b * 1e-3) / 1e9
+        out[name] = {"n": n, "ms": m_b2b, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"],
+                     "frac": ach / peaks["hbm_gbs"], "bytes_per_launch": nbytes, "launches_back_to_back": copies,
+                     "isolated_ms": m_iso, "isolated_frac": nbytes / (m_iso * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "peak_source": peaks["source"],
+                     "paper_size": name in ("vadd_2p24", "reduce_2p25")}
+        del bufs
+        torch.cuda.empty_cache()
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def nbody_mass_paths(torch, J, peaks, reps=5):
+    """One N-body step at 2^17 bodies on its two tile paths:
+    the suite's equal masses m = 1/N (11 FP32 lane-ops per interaction, m
+    factored out of every tile) and unequal masses U[0.5, 1.5)/N (the general
+    12-op path) -- device time per step from the task's CUDA events."""
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph
+    R_, W_, RW_ = J.JACC_READ, J.JACC_WRITE, J.JACC_READWRITE
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = synth.CFG5_N
+    pos, vel = synth.nbody_state(n)
+    alu = fp32_alu_tflops(peaks["sm_max_mhz"])
+    out = {}
+    for name in ("equal_mass", "general_mass"):
+        p = pos.copy()
+        if name == "general_mass":
+            p[:, 3] = (synth.uniform_f32(n, 82, 0.5, 1.5) / n).astype(np.float32)
+        dp, dv = torch.from_numpy(p).to(dev), torch.from_numpy(vel).to(dev)
+        dout = torch.empty_like(dp)
+        g, _ = make_graph(dev.index, n_streams=1)
+        g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(dp, R_, f32x4=True), g.a(dv, RW_, f32x4=True),
+                                               g.a(dout, W_, f32x4=True)],
+                   jacc.jacc_nbody_params_t(0, synth.NBODY_DT, synth.NBODY_EPS2, synth.NBODY_G))
+        ms = []
+        for i in range(reps + 1):
+            g.run()
+            if i:
                 ms.append(g.task_ms(0))
         g.destroy()
         m = statistics.mean(ms)
-        ach = nbytes / (m * 1e-3) / 1e9
-        out[name] = {"n": n, "ms": m, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"],
-                     "frac": ach / peaks["hbm_gbs"], "bytes_per_launch": nbytes, "peak_source": peaks["source"]}
-    del a, b, c, flush
-    torch.cuda.empty_cache()
+        ach = NBODY_FLOP * n * n / (m * 1e-3) / 1e12
+        out[name] = {"ms": m, "achieved": ach, "unit": "TFLOP/s", "peak": alu, "frac": ach / alu,
+                     "fp32_lane_ops_per_interaction": 11 if name == "equal_mass" else 12}
     return out
 
 
@@ -978,9 +1066,13 @@ def run_jacc(args):
     if world == 1 and not args.no_e2e:
         try:
             line["cfg1_task_graph"] = cfg1_latency(torch, J)
-            line["roofline_points_2p28"] = roofline_points(torch, J, peaks)
+            line["roofline_points"] = roofline_points(torch, J, peaks)
         except Exception as exc:   # an auxiliary measurement must not lose the bench line
             line["cfg1_task_graph"] = {"error": str(exc)[:300]}
+        try:
+            line["nbody_mass_paths"] = nbody_mass_paths(torch, J, peaks)
+        except Exception as exc:
+            line["nbody_mass_paths"] = {"error": str(exc)[:300]}
         try:
             line["next_rows"] = next_rows(torch, J, peaks)
         except Exception as exc:

@@ -183,7 +183,11 @@ typedef enum jacc_op {
      * padding, same-size output,
      *   out[y][x] = sum_{i,j} f[i][j] img[y + r - i][x + r - j].
      * args: img:R f32[H*W] (row-major), filter:R f32[(2r+1)^2],
-     * out:W f32[H*W]; params jacc_conv2d_params_t (1 <= r <= 4).           */
+     * out:W f32[H*W]; params jacc_conv2d_params_t (1 <= r <= 4).
+     * flags JACC_CONV2D_HALO_ROWS: img is a row band WITH its halos,
+     * f32[(H+2r)*W] = [r rows above][H rows][r rows below] (what
+     * JACC_OP_HALO_EXCHANGE_F32 writes), out f32[H*W] is the band's rows of
+     * the whole image's convolution (zero padding in x only).              */
     JACC_OP_CONV2D_F32 = 11,
     /* Correlation matrix (P:494 OpenBitSet "intersection
      * count", P:602 `popc`; reading R21):
@@ -197,8 +201,28 @@ typedef enum jacc_op {
      * args: row_ptr:R i32[n+1], col:R i32[nnz], val:R f32[nnz],
      * x:R f32[ncols], y:W f32[n]; params jacc_spmv_params_t.  The caller
      * guarantees 0 <= row_ptr[i] <= row_ptr[i+1] <= nnz, 0 <= col < ncols. */
-    JACC_OP_SPMV_CSR_F32 = 13
+    JACC_OP_SPMV_CSR_F32 = 13,
+    /* Halo exchange of an image split into row bands over the ranks (SURVEY
+     * §8(f) f1: 2D convolution "shards by row bands with a 2-row halo
+     * exchange").  Collective (SPMD): rank q's band is rows
+     * [lo_q, lo_q + rows) of one image, the bands of ranks 0 .. world-1
+     * consecutive and in rank order.
+     *   band:R f32[rows*W], ext:W f32[(rows+2r)*W]; params jacc_halo_params_t
+     * ext = [r rows above the band: the last r rows of rank q-1's band, zeros
+     * on rank 0][band][r rows below: the first r rows of rank q+1's band,
+     * zeros on the last rank].  rows >= r on every rank (else
+     * JACC_ERR_UNSUPPORTED on that rank).  Peer-memory form under
+     * JACC_GRAPH_P2P, ncclSend/ncclRecv otherwise, a local copy at world 1. */
+    JACC_OP_HALO_EXCHANGE_F32 = 14
 } jacc_op_t;
+
+typedef struct jacc_halo_params {
+    int64_t rows, W;        /* this rank's band rows, image columns            */
+    int32_t radius;         /* halo rows on each side (the filter radius)      */
+    int32_t reserved;
+} jacc_halo_params_t;
+
+#define JACC_CONV2D_HALO_ROWS 1u   /* jacc_conv2d_params_t.flags */
 
 typedef struct jacc_corr_params {
     int64_t ta, tb, words;  /* terms of A, terms of B, 32-bit words per term   */
@@ -211,7 +235,7 @@ typedef struct jacc_spmv_params {
 typedef struct jacc_conv2d_params {
     int64_t H, W;       /* image rows, columns                                 */
     int32_t radius;     /* filter is (2 radius + 1)^2, radius in [1, 4]        */
-    int32_t reserved;
+    uint32_t flags;     /* 0 or JACC_CONV2D_HALO_ROWS                          */
 } jacc_conv2d_params_t;
 
 typedef struct jacc_hist_params {

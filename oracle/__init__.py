@@ -211,6 +211,20 @@ def conv2d(img, filt):
     return out, ab
 
 
+def halo_band(img, lo: int, hi: int, r: int):
+    """The row band [lo, hi) of img with its r halo rows above and below,
+    zeros past the image -- what JACC_OP_HALO_EXCHANGE_F32 assembles on the
+    rank owning that band (include/jacc.h; SURVEY §8(f) f1 "shards by row
+    bands with a 2-row halo exchange").  Plain slicing, no arithmetic."""
+    img = _c(img, np.float32)
+    H, W = img.shape
+    ext = np.zeros((hi - lo + 2 * r, W), np.float32)
+    for y in range(lo - r, hi + r):
+        if 0 <= y < H:
+            ext[y - (lo - r)] = img[y]
+    return ext
+
+
 def corr_popc(A, B=None):
     """C[i][j] = sum_w popcount(A[i][w] & B[j][w]) (R21).
     A: (ta, words) uint32 bitsets; B defaults to A."""

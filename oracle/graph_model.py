@@ -46,9 +46,10 @@ OPS = {
     "conv2d": ((READ,), (READ,), (WRITE,)),
     "corr": ((READ,), (READ,), (WRITE,)),
     "spmv": ((READ,),) * 4 + ((WRITE,),),
+    "halo": ((READ,), (WRITE,)),
 }
 ATOMIC_OUT = {"reduce": 1, "hist": 1}   # arg index of the @Atomic(op=ADD) output
-COLLECTIVES = {"allreduce", "allgather", "broadcast"}
+COLLECTIVES = {"allreduce", "allgather", "broadcast", "halo"}
 
 
 @dataclass

@@ -95,44 +95,49 @@ __device__ __forceinline__ float2 abs2(float2 v) {   // sign bits cleared on the
                        __uint_as_float(__float_as_uint(v.y) & 0x7fffffffu));
 }
 
+// The APARAPI mapping computes S and K with the same FFMA of u, so they are
+// the same float and ln(S/K) = 0 EXACTLY (in the oracle's fp64 as well):
+//   d1 = (R + sigma^2/2) T / (sigma sqrt T)          -- no logarithm,
+//   S / (K e^{-RT}) = e^{RT}                          -- no division by kexp.
+// One reciprocal of q1 q2 e^{-RT} then yields 1/q1, 1/q2 and e^{RT}:
+// four MUFU ops per option (rsqrt, two ex2, one rcp) instead of six --
+// the MUFU pipe was 65 % busy (ncu) on the general form.
 // put comes from put-call parity, call - S + K e^{-RT}: an exact identity of
 // this formula (the A&S CND satisfies phi(-x) = 1 - phi(x) by construction,
 // SURVEY §8(c)-B), so it is the same value up to fp32 rounding.
-__device__ __forceinline__ void bs_price2(float2 S, float2 K, float2 T, float2 R, float2 V, float2 &call,
-                                          float2 &put) {
+__device__ __forceinline__ void bs_aparapi2(float2 u, float2 &call, float2 &put) {
     const float2 m1 = F2(-1.0f), one = F2(1.0f);
-    const float2 v2t = mul2(mul2(V, V), T);
+    const float2 S = fma2(F2(10.0f - 100.0f), u, F2(100.0f));       // = K
+    const float2 T = fma2(F2(1.0f - 10.0f), u, F2(10.0f));
+    const float2 R = fma2(F2(0.01f - 0.05f), u, F2(0.05f));
+    const float2 V = fma2(F2(0.01f - 0.10f), u, F2(0.10f));
+    const float2 v2t = mul2(mul2(V, V), T);                                            // sigma^2 T
     const float2 rs = make_float2(rsqrtf(v2t.x), rsqrtf(v2t.y));                      // 1/(sigma sqrt T)
     const float2 sst = mul2(v2t, rs);                                                  // sigma sqrt T
-    const float2 ert = mul2(mul2(R, T), F2(-1.44269504088896340736f));
-    const float2 kexp = mul2(K, make_float2(ex2_approx(ert.x), ex2_approx(ert.y)));  // K e^{-RT}
-    const float2 ratio = mul2(S, make_float2(__fdividef(1.0f, kexp.x), __fdividef(1.0f, kexp.y)));
-    const float2 lnr = mul2(make_float2(__log2f(ratio.x), __log2f(ratio.y)), F2(0.69314718055994530942f));
-    const float2 d1 = mul2(fma2(F2(0.5f), v2t, lnr), rs);
+    const float2 rt = mul2(R, T);
+    const float2 ert = mul2(rt, F2(-1.44269504088896340736f));
+    const float2 ekr = make_float2(ex2_approx(ert.x), ex2_approx(ert.y));             // e^{-RT}
+    const float2 d1 = mul2(fma2(F2(0.5f), v2t, rt), rs);
     const float2 d2 = fma2(sst, m1, d1);
     const float2 q1 = fma2(F2(0.2316419f), abs2(d1), one);
     const float2 q2 = fma2(F2(0.2316419f), abs2(d2), one);
     const float2 qq = mul2(q1, q2);
-    const float2 r = make_float2(__fdividef(1.0f, qq.x), __fdividef(1.0f, qq.y));     // both t = 1/q
+    const float2 den = mul2(qq, ekr);
+    const float2 rr = make_float2(__fdividef(1.0f, den.x), __fdividef(1.0f, den.y));  // 1/(q1 q2 e^{-RT})
+    const float2 rq = mul2(rr, ekr);                                                   // 1/(q1 q2)
+    const float2 ratio = mul2(rr, qq);                                                 // e^{RT}
     const float2 ea = mul2(mul2(F2(-0.72134752044448170368f), d1), d1);
     const float2 e1 = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));                 // e^{-d1^2/2}
     const float2 e2 = mul2(e1, ratio);                                                 // e^{-d2^2/2}
-    const float2 w1 = mul2(e1, bs_poly2(mul2(q2, r)));
-    const float2 w2 = mul2(e2, bs_poly2(mul2(q1, r)));
-    const float2 om1 = fma2(w1, m1, one), om2 = fma2(w2, m1, one);
+    const float2 w1 = mul2(e1, bs_poly2(mul2(q2, rq)));                               // t1 = 1/q1
+    const float2 w2 = mul2(e2, bs_poly2(mul2(q1, rq)));                               // t2 = 1/q2
+    // phi(d1) and -phi(d2); call = S phi(d1) - K e^{-RT} phi(d2) = S (phi(d1) -
+    // e^{-RT} phi(d2)) with K = S
+    const float2 om1 = fma2(w1, m1, one), wm2 = add2(w2, m1);
     const float2 pd1 = make_float2(d1.x < 0.f ? w1.x : om1.x, d1.y < 0.f ? w1.y : om1.y);
-    const float2 pd2 = make_float2(d2.x < 0.f ? w2.x : om2.x, d2.y < 0.f ? w2.y : om2.y);
-    call = fma2(S, pd1, mul2(mul2(kexp, m1), pd2));
-    put = add2(call, fma2(S, m1, kexp));
-}
-
-__device__ __forceinline__ void bs_aparapi2(float2 u, float2 &call, float2 &put) {
-    const float2 S = fma2(F2(10.0f - 100.0f), u, F2(100.0f));
-    const float2 K = fma2(F2(10.0f - 100.0f), u, F2(100.0f));
-    const float2 T = fma2(F2(1.0f - 10.0f), u, F2(10.0f));
-    const float2 R = fma2(F2(0.01f - 0.05f), u, F2(0.05f));
-    const float2 V = fma2(F2(0.01f - 0.10f), u, F2(0.10f));
-    bs_price2(S, K, T, R, V, call, put);
+    const float2 npd2 = make_float2(d2.x < 0.f ? -w2.x : wm2.x, d2.y < 0.f ? -w2.y : wm2.y);
+    call = mul2(S, fma2(ekr, npd2, pd1));
+    put = fma2(S, add2(ekr, m1), call);    // call - S + S e^{-RT}
 }
 
 // X = X_lo u + X_hi (1 - u) = X_hi + (X_lo - X_hi) u: one FFMA per parameter.
@@ -210,11 +215,15 @@ cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,
         // (A TMA-staged variant -- cp.async.bulk into a 4-stage mbarrier ring,
         // 8 consumer warps -- measured 163 us vs 155 us for this one: the
         // kernel is issue-bound once two loads per thread are in flight.)
+        // 3 vectors in flight per thread, 3 blocks per SM (80 registers):
+        // measured 146 us vs 149 (2, 4 blocks), 149 (4, 2), 167 (2, 1).  The
+        // grid asks for 8 blocks per SM (2.7 waves of the grid-stride loop):
+        // exactly one resident wave (148 x 3) measured slower, 146 vs 139 us.
+        // (re-measured with the 4-MUFU form: depth/blocks 3/3 137-142 us,
+        // 3/4 (16 B spills) 138-145, 2/4 142-145, 4/3 140-146)
         pick_grid(s, (n4 + 255) / 256, 8, 256, &grid, &block);
-        // 3 vectors in flight per thread, >= 3 blocks per SM (80 registers):
-        // measured 146 us vs 149 (2, 4 blocks), 149 (4, 2), 167 (2, 1)
-        bs_v4_kernel<3, 3><<<grid, block, 0, st>>>((const float4 *)u, (float4 *)call, (float4 *)put, n4,
-                                                   u + 4 * n4, call + 4 * n4, put + 4 * n4, (int)(n - 4 * n4));
+        bs_v4_kernel<3, 3><<<grid, block, 0, st>>>((const float4 *)u, (float4 *)call, (float4 *)put, n4, u + 4 * n4,
+                                                   call + 4 * n4, put + 4 * n4, (int)(n - 4 * n4));
     } else {
         pick_grid(s, (n + 255) / 256, 8, 256, &grid, &block);
         bs_scalar_kernel<<<grid, block, 0, st>>>(u, call, put, n);

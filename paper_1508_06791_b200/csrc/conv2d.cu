@@ -66,7 +66,8 @@ __device__ __forceinline__ void st_stream2(float *p, float2 v) {
 template <int R, class C>
 __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t H,
                                                             int64_t W, const float *__restrict__ filt,
-                                                            float *__restrict__ out, int tiles_x, int ntiles) {
+                                                            float *__restrict__ out, int tiles_x, int ntiles,
+                                                            int y_off) {
     constexpr int K = 2 * R + 1, BW = Box<R, C>::W, PX = C::PX, PY = C::PY, QR = C::QR, kStages = C::kStages;
     constexpr uint32_t kBytes = Box<R, C>::kBytes;
     constexpr int kStrideF = Box<R, C>::kStride / 4;         // floats between ring stages
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
         const int x0_ = ((t_) % tiles_x) * PX, y0_ = ((t_) / tiles_x) * PY;                       \
         const uint32_t b_ = tc::smem_u32(&bar[(stage_)]);                                          \
         tc::mbar_expect_tx(b_, kBytes);                                                            \
-        tc::tma_load_2d(tc::smem_u32(ring + (stage_) * kStrideF), &map, x0_ - Box<R, C>::X0, y0_ - R, b_); \
+        tc::tma_load_2d(tc::smem_u32(ring + (stage_) * kStrideF), &map, x0_ - Box<R, C>::X0, y0_ + y_off - R, b_); \
     } while (0)
     if (tid == 0) {
         tc::tma_prefetch(&map);
@@ -163,8 +164,9 @@ __global__ void __launch_bounds__(256, 2) conv2d_tma_kernel(const __grid_constan
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ img, int64_t H, int64_t W,
-                                                     const float *__restrict__ filt, float *__restrict__ out) {
+__global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ img, int64_t H_in, int64_t W,
+                                                     const float *__restrict__ filt, float *__restrict__ out,
+                                                     int64_t y_off, int64_t H) {
     constexpr int K = 2 * R + 1, SW = TX + 2 * R, SH = TY + 2 * R;
     __shared__ float s[SH][SW + 1];
     __shared__ float fs[K * K];
@@ -173,8 +175,8 @@ __global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ i
     if (threadIdx.x < K * K) fs[threadIdx.x] = filt[threadIdx.x];
     for (int idx = threadIdx.x; idx < SH * SW; idx += 256) {
         const int sy = idx / SW, sx = idx - sy * SW;
-        const int64_t gy = y0 - R + sy, gx = x0 - R + sx;
-        s[sy][sx] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? __ldg(img + gy * W + gx) : 0.f;
+        const int64_t gy = y0 + y_off - R + sy, gx = x0 - R + sx;
+        s[sy][sx] = (gy >= 0 && gy < H_in && gx >= 0 && gx < W) ? __ldg(img + gy * W + gx) : 0.f;
     }
     __syncthreads();
     float f[K * K];
@@ -205,11 +207,12 @@ __global__ void __launch_bounds__(256) conv2d_kernel(const float *__restrict__ i
 }
 
 template <int R, class C>
-cudaError_t launch_tma_cfg(const float *img, int64_t H, int64_t W, const float *filt, float *out, cudaStream_t st,
-                           bool *done) {
+cudaError_t launch_tma_cfg(const float *img, int64_t H_in, int64_t W, const float *filt, float *out,
+                           int64_t y_off, int64_t H, cudaStream_t st, bool *done) {
     *done = false;
     CUtensorMap map;
-    if (!tc::make_map_2d(&map, img, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, H, W, W * 4, Box<R, C>::H, Box<R, C>::W, 0))
+    if (!tc::make_map_2d(&map, img, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, H_in, W, W * 4, Box<R, C>::H, Box<R, C>::W,
+                         0))
         return cudaSuccess;   // no tensor map for this shape: the simple kernel runs
     const int smem = Box<R, C>::kSmem;
     cudaError_t e = set_max_dyn_smem((const void *)conv2d_tma_kernel<R, C>, smem);
@@ -217,31 +220,38 @@ cudaError_t launch_tma_cfg(const float *img, int64_t H, int64_t W, const float *
     const int64_t tiles_x = (W + C::PX - 1) / C::PX, ntiles = tiles_x * ((H + C::PY - 1) / C::PY);
     int64_t grid = (int64_t)sm_count() * blocks_per_sm((const void *)conv2d_tma_kernel<R, C>, 256, smem);
     if (grid > ntiles) grid = ntiles;
-    conv2d_tma_kernel<R, C><<<(unsigned)grid, 256, smem, st>>>(map, H, W, filt, out, (int)tiles_x, (int)ntiles);
+    conv2d_tma_kernel<R, C><<<(unsigned)grid, 256, smem, st>>>(map, H, W, filt, out, (int)tiles_x, (int)ntiles,
+                                                               (int)y_off);
     *done = true;
     return cudaGetLastError();
 }
 
 template <int R>
-cudaError_t launch_tma(const float *img, int64_t H, int64_t W, const float *filt, float *out, cudaStream_t st,
-                       bool *done) {
+cudaError_t launch_tma(const float *img, int64_t H_in, int64_t W, const float *filt, float *out, int64_t y_off,
+                       int64_t H, cudaStream_t st, bool *done) {
     // the wide tile once there are >= 16 of its tiles per SM (HBM-streaming sizes)
     const int64_t wide_tiles = ((W + CfgLarge::PX - 1) / CfgLarge::PX) * ((H + CfgLarge::PY - 1) / CfgLarge::PY);
-    if (wide_tiles >= 16 * (int64_t)sm_count()) return launch_tma_cfg<R, CfgLarge>(img, H, W, filt, out, st, done);
-    return launch_tma_cfg<R, CfgSmall>(img, H, W, filt, out, st, done);
+    if (wide_tiles >= 16 * (int64_t)sm_count())
+        return launch_tma_cfg<R, CfgLarge>(img, H_in, W, filt, out, y_off, H, st, done);
+    return launch_tma_cfg<R, CfgSmall>(img, H_in, W, filt, out, y_off, H, st, done);
 }
 
 }  // namespace
 
-cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,
-                       cudaStream_t st, int *launches) {
+// Output rows [y_off, y_off + H) of the convolution of the H_in-row image
+// (zero padded outside it), written to out rows [0, H): y_off = 0, H = H_in
+// is the plain same-size convolution; y_off = r, H_in = H + 2r convolves a
+// row band that carries its r halo rows above and below
+// (JACC_CONV2D_HALO_ROWS), so no output row touches the padding in y.
+cudaError_t conv2d_f32(const float *img, int64_t H_in, int64_t W, const float *filt, int radius, float *out,
+                       int64_t y_off, int64_t H, cudaStream_t st, int *launches) {
     if (H <= 0 || W <= 0) return cudaSuccess;
     // TMA path: 16-byte aligned rows, 8-byte aligned output (its v2 stores),
     // int32 tile coordinates
     if (radius == 2 && W % 4 == 0 && aligned16(img) && ((uintptr_t)out & 7) == 0 && (W + 128) < (1ll << 31) &&
-        (H + 64) < (1ll << 31) && ((W + 63) / 64) * ((H + 63) / 64) < (1ll << 31)) {
+        (H_in + 64) < (1ll << 31) && ((W + 63) / 64) * ((H + 63) / 64) < (1ll << 31)) {
         bool done = false;
-        cudaError_t e = launch_tma<2>(img, H, W, filt, out, st, &done);
+        cudaError_t e = launch_tma<2>(img, H_in, W, filt, out, y_off, H, st, &done);
         if (e != cudaSuccess) return e;
         if (done) {
             ++*launches;
@@ -250,10 +260,10 @@ cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt
     }
     dim3 grid((unsigned)((W + TX - 1) / TX), (unsigned)((H + TY - 1) / TY));
     switch (radius) {
-        case 1: conv2d_kernel<1><<<grid, 256, 0, st>>>(img, H, W, filt, out); break;
-        case 2: conv2d_kernel<2><<<grid, 256, 0, st>>>(img, H, W, filt, out); break;
-        case 3: conv2d_kernel<3><<<grid, 256, 0, st>>>(img, H, W, filt, out); break;
-        case 4: conv2d_kernel<4><<<grid, 256, 0, st>>>(img, H, W, filt, out); break;
+        case 1: conv2d_kernel<1><<<grid, 256, 0, st>>>(img, H_in, W, filt, out, y_off, H); break;
+        case 2: conv2d_kernel<2><<<grid, 256, 0, st>>>(img, H_in, W, filt, out, y_off, H); break;
+        case 3: conv2d_kernel<3><<<grid, 256, 0, st>>>(img, H_in, W, filt, out, y_off, H); break;
+        case 4: conv2d_kernel<4><<<grid, 256, 0, st>>>(img, H_in, W, filt, out, y_off, H); break;
         default: return cudaErrorInvalidValue;
     }
     ++*launches;

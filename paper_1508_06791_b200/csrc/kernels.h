@@ -90,8 +90,15 @@ cudaError_t peer_barrier(const PeerCtx &c, int slot, cudaStream_t st);
 constexpr int kPeerBarrierSlot = kPeerSlots - 1;   // reserved: collective tasks use 0 .. kPeerSlots - 2
 
 // 2D convolution
-cudaError_t conv2d_f32(const float *img, int64_t H, int64_t W, const float *filt, int radius, float *out,
-                       cudaStream_t st, int *launches);
+cudaError_t conv2d_f32(const float *img, int64_t H_in, int64_t W, const float *filt, int radius, float *out,
+                       int64_t y_off, int64_t H, cudaStream_t st, int *launches);
+// JACC_OP_HALO_EXCHANGE_F32 (row bands of an image, SPMD): ext = [r rows of
+// the band above][band][r rows of the band below], zeros past the image
+size_t peer_halo_stage_bytes(int64_t W, int radius);
+cudaError_t peer_halo(const PeerOp &op, const float *band, float *ext, int64_t rows, int64_t W, int radius,
+                      cudaStream_t st, int *launches);
+cudaError_t halo_local(const float *band, float *ext, int64_t rows, int64_t W, int radius, bool top_zero,
+                       bool bottom_zero, cudaStream_t st, int *launches);
 
 // correlation matrix
 size_t corr_ws_bytes(int64_t ta, int64_t tb, int64_t words);

@@ -8,6 +8,8 @@
 // Every rank's kernel both sends (stores into the peers' windows) and
 // receives (waits for the peers' data flags), so a task's completion event
 // means the result is in place on this rank, like the NCCL call it replaces.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "peer.cuh"
@@ -96,6 +98,72 @@ __global__ void barrier_kernel(PeerCtx c, int slot) {
     peer::wait_all_data(c, slot, e);
 }
 
+// Halo exchange of row bands (JACC_OP_HALO_EXCHANGE_F32, SURVEY §8(f) f1:
+// "shards by row bands with a 2-row halo exchange").  Rank q's band is rows
+// [lo_q, lo_q + rows) of one image; ext = [r rows above][band][r rows below].
+// A rank does not know its neighbours' band heights, so it does not store
+// into their ext directly: it pushes its first r rows into rank q-1's
+// staging "from below" and its last r rows into rank q+1's staging "from
+// above" (fixed window offsets, same on every rank), publishes, and the
+// finish kernel copies its two staging slots into its own ext halos.
+// Staging is double-buffered by epoch parity (the allreduce argument: a rank
+// cannot write epoch e+2 before every rank signalled e+1, which each does
+// only after its finish kernel of epoch e read the staging).
+__global__ void __launch_bounds__(kBlock) halo_push_kernel(PeerCtx c, int slot, int64_t stage_off,
+                                                           const float *band, float *ext, int64_t rows, int64_t W,
+                                                           int r) {
+    const uint64_t e = peer::epoch(c, slot);
+    const size_t edge = (size_t)r * W * 4, par = (size_t)stage_off + (e & 1) * 2 * edge;
+    const size_t body = (size_t)rows * W * 4;
+    // this rank's band into the middle of its own ext (grid-wide slices)
+    const size_t per = (body / gridDim.x + 15) & ~(size_t)15;
+    const size_t lo = per * blockIdx.x < body ? per * blockIdx.x : body;
+    const size_t hi = lo + per < body ? lo + per : body;
+    peer::block_copy((char *)ext + edge + lo, (const char *)band + lo, hi - lo, threadIdx.x, blockDim.x);
+    // edges to the neighbours' staging (block 0 only: 2 x r rows)
+    if (blockIdx.x == 0) {
+        peer::for_each_rank(c, [&](int q, char *b) {
+            if (q == c.rank - 1)        // rank above receives our first r rows as "from below"
+                peer::block_copy(b + par + edge, (const char *)band, edge, threadIdx.x, blockDim.x);
+            else if (q == c.rank + 1)   // rank below receives our last r rows as "from above"
+                peer::block_copy(b + par, (const char *)band + body - edge, edge, threadIdx.x, blockDim.x);
+        });
+    }
+    if (peer::grid_last(c, slot) && threadIdx.x == 0) peer::publish_data(c, slot, e);
+}
+
+__global__ void __launch_bounds__(kBlock) halo_finish_kernel(PeerCtx c, int slot, int64_t stage_off, float *ext,
+                                                             int64_t rows, int64_t W, int r) {
+    const uint64_t e = *(volatile uint64_t *)peer::count(c, slot);   // bumped by the push kernel
+    peer::wait_all_data(c, slot, e);
+    __syncthreads();
+    const size_t edge = (size_t)r * W * 4, par = (size_t)stage_off + (e & 1) * 2 * edge;
+    const int64_t n = (int64_t)r * W;
+    float *top = ext, *bot = ext + (size_t)(r + rows) * W;
+    const float *from_above = (const float *)(c.self + par), *from_below = (const float *)(c.self + par + edge);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        top[i] = c.rank > 0 ? __ldcg(from_above + i) : 0.f;
+        bot[i] = c.rank < c.world - 1 ? __ldcg(from_below + i) : 0.f;
+    }
+}
+
+// One rank (world 1, or the NCCL path's local part): band into the middle,
+// zeros for the halos past the image.
+__global__ void __launch_bounds__(kBlock) halo_local_kernel(const float *band, float *ext, int64_t rows, int64_t W,
+                                                            int r, int top_zero, int bottom_zero) {
+    const int64_t n = (int64_t)rows * W, h = (int64_t)r * W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n + 2 * h;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < h) {
+            if (top_zero) ext[i] = 0.f;
+        } else if (i < h + n) {
+            ext[i] = __ldg(band + (i - h));
+        } else if (bottom_zero) {
+            ext[i] = 0.f;
+        }
+    }
+}
+
 int copy_grid(int64_t bytes) {
     // ~64 KiB per block, at most 32 blocks (a few SMs: the copy is NVLink-bound)
     int64_t g = (bytes + (64 << 10) - 1) / (64 << 10);
@@ -125,6 +193,28 @@ cudaError_t peer_allreduce(const PeerOp &op, void *buf, int64_t n, bool is_int, 
         allreduce_sum_kernel<float><<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, (float *)buf, n);
     }
     *launches += 2;
+    return cudaGetLastError();
+}
+
+size_t peer_halo_stage_bytes(int64_t W, int radius) { return 2 * 2 * (size_t)radius * W * 4; }
+
+cudaError_t peer_halo(const PeerOp &op, const float *band, float *ext, int64_t rows, int64_t W, int radius,
+                      cudaStream_t st, int *launches) {
+    const int64_t bytes = rows * W * 4;
+    const int g = (int)std::min<int64_t>(148, std::max<int64_t>(1, bytes / (256 << 10)));
+    halo_push_kernel<<<g, kBlock, 0, st>>>(op.ctx, op.slot, op.off, band, ext, rows, W, radius);
+    const int g2 = (int)std::min<int64_t>(32, std::max<int64_t>(1, (int64_t)radius * W / 8192));
+    halo_finish_kernel<<<g2, kBlock, 0, st>>>(op.ctx, op.slot, op.off, ext, rows, W, radius);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t halo_local(const float *band, float *ext, int64_t rows, int64_t W, int radius, bool top_zero,
+                       bool bottom_zero, cudaStream_t st, int *launches) {
+    const int64_t n = (rows + 2 * radius) * W;
+    const int g = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (n + kBlock * 4 - 1) / (kBlock * 4)));
+    halo_local_kernel<<<g, kBlock, 0, st>>>(band, ext, rows, W, radius, top_zero, bottom_zero);
+    ++*launches;
     return cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ __device__ __forceinline__ float block_sum(float v, float *sh) {
 // c and summed in the very same order as reduce_kernel<false> on c -- so the
 // merged pair produces bit-identical c and s in one pass over a and b.
 template <bool kFused, bool kPeer>
-__global__ void __launch_bounds__(kBlock) reduce_kernel(const float *__restrict__ x, const float *__restrict__ xb,
+__global__ void __launch_bounds__(kBlock, 2) reduce_kernel(const float *__restrict__ x, const float *__restrict__ xb,
                                                         float *__restrict__ xc, int64_t n, int64_t head,
                                                         float *__restrict__ out, float *__restrict__ partials,
                                                         unsigned *__restrict__ ticket, int assign, PeerOp pop) {
@@ -117,7 +117,12 @@ size_t reduce_ws_bytes(int64_t) { return sizeof(float) * kMaxGrid + 128; }
 
 namespace {
 void reduce_grid(int64_t n, const jacc_schedule_t *s, int *grid, int *block) {
-    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), kPerSm, kBlock, grid, block);   // small n: more blocks
+    // one resident wave: with <= 64 registers (launch bounds) 2 blocks of
+    // 512 fit per SM, not kPerSm -- a grid of 4 per SM ran as two waves (the
+    // second starting as the first drained).  The same grid for every
+    // instantiation: the merged vadd+reduce must sum in the plain order.
+    static const int occ = blocks_per_sm((const void *)reduce_kernel<false, false>, kBlock, 0);
+    pick_grid(s, (n / 4 + kBlock * 2 - 1) / (kBlock * 2), occ < kPerSm ? occ : kPerSm, kBlock, grid, block);
     *block = kBlock;   // the block tree assumes kBlock threads
     if (*grid > kMaxGrid) *grid = kMaxGrid;
 }

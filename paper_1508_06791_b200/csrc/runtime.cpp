@@ -63,12 +63,14 @@ const char *op_name(int op) {
         case JACC_OP_CONV2D_F32: return "conv2d";
         case JACC_OP_CORR_POPC_U32: return "corr";
         case JACC_OP_SPMV_CSR_F32: return "spmv";
+        case JACC_OP_HALO_EXCHANGE_F32: return "halo";
         default: return "?";
     }
 }
 
 bool is_collective(int op) {
-    return op == JACC_OP_ALLREDUCE_SUM || op == JACC_OP_ALLGATHER || op == JACC_OP_BROADCAST;
+    return op == JACC_OP_ALLREDUCE_SUM || op == JACC_OP_ALLGATHER || op == JACC_OP_BROADCAST ||
+           op == JACC_OP_HALO_EXCHANGE_F32;
 }
 
 // index of the @Atomic(op=ADD) output of an op (auto-zeroed in W mode), or -1
@@ -316,6 +318,18 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             if (a[1].count != a[0].count * (uint64_t)g->cfg.world)
                 return fail(JACC_ERR_INVALID_ARG, "allgather: recv count != send count * world");
             break;
+        case JACC_OP_HALO_EXCHANGE_F32: {
+            T(need(2)); T(acc(0, R)); T(acc(1, W)); T(dt(0, JACC_F32)); T(dt(1, JACC_F32));
+            if (!params || psz < sizeof(jacc_halo_params_t)) return fail(JACC_ERR_INVALID_ARG, "halo: params");
+            const jacc_halo_params_t *p = (const jacc_halo_params_t *)params;
+            if (p->radius < 1 || p->rows < 0 || p->W < 0 || a[0].count != (uint64_t)p->rows * (uint64_t)p->W ||
+                a[1].count != (uint64_t)(p->rows + 2 * p->radius) * (uint64_t)p->W)
+                return fail(JACC_ERR_INVALID_ARG, "halo: counts do not match rows, W, radius");
+            if (p->rows < p->radius && g->cfg.world > 1)
+                return fail(JACC_ERR_UNSUPPORTED, "halo: band of %lld rows < radius %d",
+                            (long long)p->rows, p->radius);
+            break;
+        }
         case JACC_OP_BROADCAST: {
             T(need(1)); T(acc(0, RW));
             if (!params || psz < sizeof(jacc_bcast_params_t)) return fail(JACC_ERR_INVALID_ARG, "broadcast: params");
@@ -330,8 +344,10 @@ int validate(const jacc_graph *g, int op, const jacc_arg_t *a, int n, const void
             const jacc_conv2d_params_t *p = (const jacc_conv2d_params_t *)params;
             if (p->radius < 1 || p->radius > 4) return fail(JACC_ERR_UNSUPPORTED, "conv2d: radius %d", p->radius);
             const uint64_t k = 2 * p->radius + 1;
-            if (p->H < 0 || p->W < 0 || a[0].count != (uint64_t)p->H * (uint64_t)p->W || a[2].count != a[0].count ||
-                a[1].count != k * k)
+            if (p->flags & ~JACC_CONV2D_HALO_ROWS) return fail(JACC_ERR_INVALID_ARG, "conv2d: unknown flags");
+            const uint64_t h_in = (uint64_t)p->H + ((p->flags & JACC_CONV2D_HALO_ROWS) ? 2 * p->radius : 0);
+            if (p->H < 0 || p->W < 0 || a[0].count != h_in * (uint64_t)p->W ||
+                a[2].count != (uint64_t)p->H * (uint64_t)p->W || a[1].count != k * k)
                 return fail(JACC_ERR_INVALID_ARG, "conv2d: counts do not match H x W / filter size");
             break;
         }
@@ -423,6 +439,7 @@ double est_cost(const jacc_graph *g, const Task &T) {
         }
         case JACC_OP_NBODY_STEP_F32: return 20.0 * a[0].count * a[1].count / alu;
         case JACC_OP_CONV2D_F32: return 8.0 * a[0].count / hbm;
+        case JACC_OP_HALO_EXCHANGE_F32: return 8.0 * a[0].count / hbm;
         case JACC_OP_CORR_POPC_U32: {
             const jacc_corr_params_t *p = (const jacc_corr_params_t *)T.params.data();
             return 3.0 * p->ta * p->tb * p->words / alu;
@@ -689,6 +706,14 @@ int prepare_peer(jacc_graph *g) {
             }
             continue;
         }
+        if (T.op == JACC_OP_HALO_EXCHANGE_F32) {   // staging for the neighbours' edge rows
+            if (T.peer_off < 0) {
+                const jacc_halo_params_t *hp = (const jacc_halo_params_t *)T.params.data();
+                T.peer_off = win_alloc(g, jacc_k::peer_halo_stage_bytes(hp->W, hp->radius));
+                if (T.peer_off < 0) return fail(JACC_ERR_OOM, "P2P window full (halo staging)");
+            }
+            continue;
+        }
         Buffer &B = g->bufs[T.args[T.op == JACC_OP_ALLGATHER ? 1 : 0].buf];
         if (B.device) {
             if (win_off(g, B.dptr, B.bytes) < 0)
@@ -765,7 +790,7 @@ jacc_k::PeerOp peer_op(const jacc_graph *g, const Task &C) {
     jacc_k::PeerOp op{};
     op.ctx = peer_ctx(g);
     op.slot = C.slot;
-    if (C.op == JACC_OP_ALLREDUCE_SUM) op.off = C.peer_off;
+    if (C.op == JACC_OP_ALLREDUCE_SUM || C.op == JACC_OP_HALO_EXCHANGE_F32) op.off = C.peer_off;
     else {
         const Buffer &B = g->bufs[C.args[C.op == JACC_OP_ALLGATHER ? 1 : 0].buf];
         op.off = win_off(g, B.dptr, B.bytes);
@@ -821,8 +846,10 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
             break;
         case JACC_OP_CONV2D_F32: {
             const jacc_conv2d_params_t *cp = (const jacc_conv2d_params_t *)T.params.data();
-            e = jacc_k::conv2d_f32((const float *)P(0), cp->H, cp->W, (const float *)P(1), cp->radius, (float *)P(2),
-                                   st, launches);
+            const bool halo = cp->flags & JACC_CONV2D_HALO_ROWS;
+            e = jacc_k::conv2d_f32((const float *)P(0), cp->H + (halo ? 2 * cp->radius : 0), cp->W,
+                                   (const float *)P(1), cp->radius, (float *)P(2), halo ? cp->radius : 0, cp->H, st,
+                                   launches);
             break;
         }
         case JACC_OP_CORR_POPC_U32: {
@@ -837,6 +864,27 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
                                      ((const jacc_spmv_params_t *)T.params.data())->n, (int64_t)a[1].count, st,
                                      launches);
             break;
+        case JACC_OP_HALO_EXCHANGE_F32: {
+            const jacc_halo_params_t *hp = (const jacc_halo_params_t *)T.params.data();
+            const float *band = (const float *)P(0);
+            float *ext = (float *)P(1);
+            const int rk = g->cfg.rank, wd = g->cfg.world;
+            if (hp->rows * hp->W == 0 && wd == 1) break;
+            if (p2p(g) && wd > 1) {
+                e = jacc_k::peer_halo(peer_op(g, T), band, ext, hp->rows, hp->W, hp->radius, st, launches);
+                break;
+            }
+            // world 1, or NCCL: band into the middle, zeros past the image,
+            // then the neighbours' rows by ncclSend / ncclRecv
+            e = jacc_k::halo_local(band, ext, hp->rows, hp->W, hp->radius, rk == 0, rk == wd - 1, st, launches);
+            if (e != cudaSuccess || wd == 1) break;
+            const uint64_t edge = (uint64_t)hp->radius * hp->W;
+            const int r = jacc_nccl::halo_exchange(band, band + (hp->rows * hp->W - edge), ext,
+                                                   ext + (hp->rows + hp->radius) * hp->W, edge, rk, wd,
+                                                   g->cfg.nccl_comm, st);
+            if (r != 0) return fail(JACC_ERR_NCCL, "halo: %s", jacc_nccl::last_error());
+            break;
+        }
         case JACC_OP_ALLREDUCE_SUM:
         case JACC_OP_ALLGATHER:
         case JACC_OP_BROADCAST: {
@@ -1186,6 +1234,7 @@ size_t jacc_abi_sizeof(const char *name) {
     S(jacc_arg_t); S(jacc_schedule_t); S(jacc_config_t); S(jacc_stats_t);
     S(jacc_hist_params_t); S(jacc_sgemm_params_t); S(jacc_nbody_params_t); S(jacc_bcast_params_t);
     S(jacc_conv2d_params_t); S(jacc_corr_params_t); S(jacc_spmv_params_t); S(jacc_peer_handle_t);
+    S(jacc_halo_params_t);
 #undef S
     return 0;
 }

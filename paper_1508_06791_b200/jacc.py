@@ -39,7 +39,8 @@ JACC_ABI_VERSION = 2
 (JACC_OP_VADD_F32, JACC_OP_REDUCE_SUM_F32, JACC_OP_HISTOGRAM_I32, JACC_OP_BLACKSCHOLES_F32,
  JACC_OP_BLACKSCHOLES_SOA_F32, JACC_OP_SGEMM_F32, JACC_OP_NBODY_STEP_F32, JACC_OP_ALLREDUCE_SUM,
  JACC_OP_ALLGATHER, JACC_OP_BROADCAST, JACC_OP_CONV2D_F32, JACC_OP_CORR_POPC_U32,
- JACC_OP_SPMV_CSR_F32) = range(1, 14)
+ JACC_OP_SPMV_CSR_F32, JACC_OP_HALO_EXCHANGE_F32) = range(1, 15)
+JACC_CONV2D_HALO_ROWS = 1
 JACC_SGEMM_3XTF32, JACC_SGEMM_FFMA = 0, 1
 STATE_NAMES = {0: "BUILDING", 1: "EXECUTING", 2: "DONE", 3: "FAILED"}
 DTYPE_SIZE = {JACC_F32: 4, JACC_I32: 4, JACC_F32X4: 16}
@@ -103,6 +104,11 @@ class jacc_bcast_params_t(ctypes.Structure):
 
 class jacc_conv2d_params_t(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int64), ("W", ctypes.c_int64), ("radius", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class jacc_halo_params_t(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("W", ctypes.c_int64), ("radius", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -123,7 +129,8 @@ STRUCTS = {"jacc_peer_handle_t": jacc_peer_handle_t, "jacc_corr_params_t": jacc_
            "jacc_arg_t": jacc_arg_t, "jacc_schedule_t": jacc_schedule_t, "jacc_config_t": jacc_config_t,
            "jacc_stats_t": jacc_stats_t, "jacc_hist_params_t": jacc_hist_params_t,
            "jacc_sgemm_params_t": jacc_sgemm_params_t, "jacc_nbody_params_t": jacc_nbody_params_t,
-           "jacc_bcast_params_t": jacc_bcast_params_t, "jacc_conv2d_params_t": jacc_conv2d_params_t}
+           "jacc_bcast_params_t": jacc_bcast_params_t, "jacc_conv2d_params_t": jacc_conv2d_params_t,
+           "jacc_halo_params_t": jacc_halo_params_t}
 
 # ------------------------------------------------------------- entry points
 _vp = ctypes.c_void_p

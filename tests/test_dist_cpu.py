@@ -68,6 +68,28 @@ def _worker(rank, world, port, q):
             P = torch.cat(gathered).numpy()
         fp, fv = oracle.nbody_steps(pos, vel, steps)
         res["nbody"] = bool(np.array_equal(P, fp) and np.array_equal(V, fv[lo:hi]))
+        # f1: 2D convolution by row bands, r halo rows exchanged with the
+        # neighbours (point-to-point, the NCCL path's ncclSend/ncclRecv),
+        # then the band's rows of the convolution -> bitwise the full image's
+        H, Wd, r = 61, 17, 2
+        img = synth.uniform_f32(H * Wd, 95, -1, 1).reshape(H, Wd)
+        f = synth.uniform_f32(25, 96, -1, 1).reshape(5, 5)
+        blo, bhi = synth.shard_range(H, rank, world)
+        band = torch.from_numpy(img[blo:bhi].copy())
+        top = torch.zeros((r, Wd)); bot = torch.zeros((r, Wd))
+        ops = []
+        if rank > 0:
+            ops += [dist.P2POp(dist.isend, band[:r].contiguous(), rank - 1),
+                    dist.P2POp(dist.irecv, top, rank - 1)]
+        if rank < world - 1:
+            ops += [dist.P2POp(dist.isend, band[-r:].contiguous(), rank + 1),
+                    dist.P2POp(dist.irecv, bot, rank + 1)]
+        for w_ in dist.batch_isend_irecv(ops):
+            w_.wait()
+        ext = torch.cat([top, band, bot]).numpy()
+        res["halo_ext"] = bool(np.array_equal(ext, oracle.halo_band(img, blo, bhi, r)))
+        o, _ = oracle.conv2d(ext, f)
+        res["conv_band"] = bool(np.array_equal(o[r:r + bhi - blo], oracle.conv2d(img, f)[0][blo:bhi]))
         # each rank's libjacc plan with world = 2: counted copies per rank
         import paper_1508_06791_b200 as J
         from paper_1508_06791_b200 import jacc
@@ -127,6 +149,7 @@ def test_spmd_world2_gloo():
     for r in range(world):
         assert "error" not in out[r], out[r].get("error")
         assert out[r]["hist"] and out[r]["reduce"] and out[r]["sgemm"] and out[r]["nbody"], out[r]
+        assert out[r]["halo_ext"] and out[r]["conv_band"], out[r]
         assert out[r]["plan"] == (2, 3, 10, 10), out[r]["plan"]
         # hist+allreduce, reduce+allreduce, 9 nbody+allgather (the first allgather has no producer)
         assert out[r]["p2p_fuse"] == (11, True), out[r]["p2p_fuse"]

@@ -204,3 +204,37 @@ def test_corr_replayed_graph_bit_exact(same):
         assert np.array_equal(C, oracle.corr_popc(A, B)), it
     assert g.stats()["graph_replays"] >= 1
     g.destroy()
+
+
+# ------------------------------------------- f1 row-band sharding (halo rows)
+def _conv_band_graph(g, band, f, rows, Wd, r):
+    """halo exchange of the band, then conv2d of the extended band."""
+    ext = np.zeros((rows + 2 * r, Wd), np.float32)
+    out = np.zeros((rows, Wd), np.float32)
+    g.add_task(J.JACC_OP_HALO_EXCHANGE_F32, [g.a(band, R), g.a(ext, W)], jacc.jacc_halo_params_t(rows, Wd, r, 0))
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(ext, R), g.a(f, R), g.a(out, W)],
+               jacc.jacc_conv2d_params_t(rows, Wd, r, J.JACC_CONV2D_HALO_ROWS))
+    return ext, out
+
+
+@pytest.mark.parametrize("shape,r", [((300, 256), 2), ((300, 250), 2), ((77, 64), 1), ((2048, 2048), 2), ((65, 40), 4)])
+def test_conv2d_halo_rows_world1(shape, r):
+    """World 1: the halo exchange gives [zeros][image][zeros] and the halo-row
+    convolution equals the plain same-size convolution bit for bit (TMA path
+    for W % 4 == 0 and r == 2, the simple kernel otherwise) and the oracle."""
+    H, Wd = shape
+    img = synth.uniform_f32(H * Wd, 700 + H, -1, 1).reshape(H, Wd)
+    f = synth.uniform_f32((2 * r + 1) ** 2, 701, -1, 1).reshape(2 * r + 1, 2 * r + 1)
+    g, _ = make_graph(0)
+    ext, out = _conv_band_graph(g, img, f, H, Wd, r)
+    g.run()
+    g.destroy()
+    assert np.array_equal(ext, oracle.halo_band(img, 0, H, r))
+    plain = np.zeros_like(img)
+    g, _ = make_graph(0)
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(plain, W)], jacc.jacc_conv2d_params_t(H, Wd, r, 0))
+    g.run()
+    g.destroy()
+    assert np.array_equal(out, plain)
+    ref, ab = oracle.conv2d(img, f)
+    assert np.all(np.abs(out.astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)

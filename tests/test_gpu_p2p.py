@@ -304,6 +304,87 @@ def test_p2p_nbody_gather_not_fused_when_unsafe():
         assert (al["launches"], sw["launches"]) == (3, 4), (al["launches"], sw["launches"])
 
 
+def _halo_worker(rank, world, port, q, cases):
+    """2D convolution sharded by row bands: each rank holds
+    its band, exchanges r halo rows with its neighbours over the peer windows
+    (JACC_OP_HALO_EXCHANGE_F32) and convolves its extended band
+    (JACC_CONV2D_HALO_ROWS); three epochs (both staging parities)."""
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import synth
+        import paper_1508_06791_b200 as J
+        from paper_1508_06791_b200 import jacc
+        from paper_1508_06791_b200.torch_glue import make_graph, peer_setup
+        res = {}
+        for (H, Wd, r, flags) in cases:
+            img = synth.uniform_f32(H * Wd, 710 + H, -1, 1).reshape(H, Wd)
+            f = synth.uniform_f32((2 * r + 1) ** 2, 711, -1, 1).reshape(2 * r + 1, 2 * r + 1)
+            lo, hi = synth.shard_range(H, rank, world)
+            g, _ = make_graph(0, rank=rank, world=world, flags=J.JACC_GRAPH_P2P | flags)
+            peer_setup(g, 4 << 20)
+            band = pinned(img[lo:hi])
+            ext = pinned(np.zeros((hi - lo + 2 * r, Wd), np.float32))
+            out = pinned(np.zeros((hi - lo, Wd), np.float32))
+            g.add_task(J.JACC_OP_HALO_EXCHANGE_F32, [g.a(band, R), g.a(ext, W)],
+                       jacc.jacc_halo_params_t(hi - lo, Wd, r, 0))
+            g.add_task(J.JACC_OP_CONV2D_F32, [g.a(ext, R), g.a(f, R), g.a(out, W)],
+                       jacc.jacc_conv2d_params_t(hi - lo, Wd, r, J.JACC_CONV2D_HALO_ROWS))
+            outs = []
+            for it in range(3):
+                g.run()
+                outs.append((ext.copy(), out.copy()))
+            res[(H, Wd, r, flags)] = (outs, g.stats()["launches"])
+            g.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_conv2d_row_bands(world):
+    """Every rank's halo rows equal oracle.halo_band and its output rows equal
+    the single-GPU convolution of the whole image bit for bit (same kernel,
+    same per-pixel sum order), three epochs, direct and replayed."""
+    import torch.multiprocessing as mp
+    from paper_1508_06791_b200.torch_glue import make_graph
+    cases = [(1030, 256, 2, 0), (515, 250, 2, J.JACC_GRAPH_REPLAY), (2048, 2048, 2, 0), (90, 72, 4, 0)]
+    port = 29500 + (os.getpid() % 90) + 3 * world
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, qu, cases)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(qu.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for (H, Wd, r, flags) in cases:
+        img = synth.uniform_f32(H * Wd, 710 + H, -1, 1).reshape(H, Wd)
+        f = synth.uniform_f32((2 * r + 1) ** 2, 711, -1, 1).reshape(2 * r + 1, 2 * r + 1)
+        full = np.zeros_like(img)
+        g, _ = make_graph(0)
+        g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(full, W)],
+                   jacc.jacc_conv2d_params_t(H, Wd, r, 0))
+        g.run()
+        g.destroy()
+        ref, ab = oracle.conv2d(img, f)
+        assert np.all(np.abs(full.astype(np.float64) - ref) <= 1e-5 * ab + 1e-30)
+        for rk in range(world):
+            assert "error" not in out[rk], out[rk].get("error")
+            outs, launches = out[rk][(H, Wd, r, flags)]
+            lo, hi = synth.shard_range(H, rk, world)
+            for it, (ext, o) in enumerate(outs):
+                assert np.array_equal(ext, oracle.halo_band(img, lo, hi, r)), (H, rk, it)
+                assert np.array_equal(o, full[lo:hi]), (H, rk, it)
+
+
 def test_p2p_window_errors():
     """Error paths of the peer windows (include/jacc.h): a full window is
     JACC_ERR_OOM, handles whose window sizes differ are JACC_ERR_INVALID_ARG

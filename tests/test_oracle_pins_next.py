@@ -3,6 +3,7 @@ import numpy as np
 import pytest
 from scipy.signal import convolve2d
 
+import oracle
 import synth
 
 
@@ -105,3 +106,38 @@ def test_banded_csr_is_symmetric_pattern_with_diagonal():
     pattern = set(zip(rows.tolist(), col.tolist()))
     assert all((j, i) in pattern for i, j in pattern)
     assert all((i, i) in pattern for i in range(300))
+
+
+# --------------------------------------------- halo bands (f1 row sharding)
+@pytest.mark.parametrize("H,P,r", [(37, 2, 2), (40, 4, 2), (9, 3, 1), (50, 8, 4)])
+def test_halo_band_pins(H, P, r):
+    """oracle.halo_band: the bands' middle rows tile the image; a band's top
+    halo is the previous band's last r rows (zeros above row 0), its bottom
+    halo the next band's first r rows (zeros below the last row); and the
+    convolution of every extended band, middle rows, reassembles the
+    whole-image convolution exactly (each output row reads only rows within
+    r of it)."""
+    import synth
+    img = synth.uniform_f32(H * 13, 90 + H, -1, 1).reshape(H, 13)
+    f = synth.uniform_f32((2 * r + 1) ** 2, 91, -1, 1).reshape(2 * r + 1, 2 * r + 1)
+    full, _ = oracle.conv2d(img, f)
+    mids, outs = [], []
+    for q in range(P):
+        lo, hi = synth.shard_range(H, q, P)
+        ext = oracle.halo_band(img, lo, hi, r)
+        assert ext.shape == (hi - lo + 2 * r, 13)
+        mids.append(ext[r:r + hi - lo])
+        top, bot = ext[:r], ext[r + hi - lo:]
+        if q == 0:
+            assert not top.any()
+        else:
+            plo, phi = synth.shard_range(H, q - 1, P)
+            assert np.array_equal(top, img[phi - r:phi])
+        if q == P - 1:
+            assert not bot.any()
+        else:
+            assert np.array_equal(bot, img[hi:hi + r])
+        o, _ = oracle.conv2d(ext, f)
+        outs.append(o[r:r + hi - lo])
+    assert np.array_equal(np.concatenate(mids), img)
+    assert np.array_equal(np.concatenate(outs), full)
