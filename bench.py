@@ -361,7 +361,9 @@ class CpuSample:
     cfg1 (2^20), cfg2 (2^28 keys) and cfg3 (2^26 options) run at FULL size;
     cfg4 runs 2 x threads rows of the 8192^3 product (each thread gets two
     whole rows) and cfg5 16 x threads targets of one 2^17-body step; those two
-    are scaled linearly to the full graph (flagged "extrapolated").  The
+    are scaled linearly to the full graph (flagged "extrapolated").  (64 x
+    threads targets: ~25 ms of work; 16 x threads, ~6 ms, read 2x apart
+    between two processes.)  The
     oracle's vadd / reduce / histogram loops are single-threaded, the
     Black-Scholes, SGEMM and N-body loops use OpenMP over independent outer
     indices: each part reports the threads it used.  Inputs are generated
@@ -380,7 +382,7 @@ class CpuSample:
         self.A, self.B = synth.sgemm_inputs(self.rows, n4, n4)
         pos, _ = synth.nbody_state(synth.CFG5_N)
         self.p64 = pos.astype(np.float64)
-        self.ntg = 16 * self.threads
+        self.ntg = 64 * self.threads
 
     def run(self, threads=None, small=False):
         """{part: {"s": measured seconds, "scale": factor to the full graph,
@@ -1082,7 +1084,15 @@ def run_jacc(args):
         except Exception as exc:
             line["paper_protocol"] = {"error": str(exc)[:300]}
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline_leg()
+        # in a fresh process, like the reference arm: this one holds torch's
+        # OpenMP pool and CUDA threads, which skewed the small OpenMP samples
+        # (cfg5 read 2x slower here than in the reference arm's process)
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-json"],
+                               capture_output=True, text=True, timeout=900)
+            line["cpu_baseline"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:
+            line["cpu_baseline"] = {"error": str(exc)[:300]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -1115,7 +1125,11 @@ def main():
                     help="N>1 collectives: fused NVLink peer-memory kernels (default) or NCCL calls")
     ap.add_argument("--no-replay", dest="replay", action="store_false",
                     help="issue every action from the host each step instead of replaying the captured plan")
+    ap.add_argument("--cpu-baseline-json", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_baseline_json:
+        print(json.dumps(cpu_baseline_leg()), flush=True)
+        return 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-run under torchrun instead of silently
         # measuring one rank (the N-rank launch is the contract's)

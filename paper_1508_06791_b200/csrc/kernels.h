@@ -56,9 +56,11 @@ cudaError_t vadd_reduce_f32(const float *a, const float *b, float *c, int64_t n,
 
 // bins[k] += #{keys == k}
 size_t histogram_ws_bytes(int64_t n, int nbins);
+// assign: bins = counts (a W output, instead of a memset + add); else bins += counts
 cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbins, void *ws,
                           const jacc_schedule_t *s, cudaStream_t st, int *launches,
-                          const PeerOp *allreduce = nullptr);   // fused allreduce(bins), nbins <= 256, n > 0
+                          const PeerOp *allreduce = nullptr,   // fused allreduce(bins), nbins <= 256, n > 0
+                          bool assign = false);
 
 // APARAPI Black-Scholes
 cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,

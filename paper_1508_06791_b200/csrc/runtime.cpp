@@ -824,7 +824,7 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
         case JACC_OP_HISTOGRAM_I32:
             e = jacc_k::histogram_i32((const int32_t *)P(0), (int64_t)a[0].count, (int32_t *)P(1),
                                       ((const jacc_hist_params_t *)T.params.data())->nbins, T.ws, sched, st,
-                                      launches, fp);
+                                      launches, fp, assign);
             break;
         case JACC_OP_BLACKSCHOLES_F32:
             e = jacc_k::blackscholes_f32((const float *)P(0), (float *)P(1), (float *)P(2), (int64_t)a[0].count,
@@ -1060,12 +1060,16 @@ int issue(jacc_graph *g) {
             if (timing)
                 for (int t : grp) CK(rec(g->tasks[t].ev_start));
             // MEMSET0 actions (auto-zero of @Atomic outputs) of the
-            // group's tasks; a reduction's single float is instead assigned
-            // (not added) by its kernel -- one memset node less per task
+            // group's tasks; a reduction's sum and a histogram's bins are
+            // instead assigned (not added) by their kernels' last block --
+            // one memset node less per task
             bool assign = false;
             for (int t : grp)
                 for (int b : g->memset_bufs[t]) {
-                    if (g->tasks[t].op == JACC_OP_REDUCE_SUM_F32) { assign = true; continue; }
+                    if (g->tasks[t].op == JACC_OP_REDUCE_SUM_F32 || g->tasks[t].op == JACC_OP_HISTOGRAM_I32) {
+                        assign = true;
+                        continue;
+                    }
                     CK(cudaMemsetAsync(g->bufs[b].dptr, 0, g->bufs[b].bytes, st));
                 }
             int rc;
