@@ -39,6 +39,17 @@ g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits2.view(np.int32), R), g.a(bits2.vie
 g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A2, R), g.a(B2, R), g.a(C2, W)], jacc.jacc_sgemm_params_t(300, 520, 1000, 1000, 520, 520, 0, 0))
 g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(pos3, R, f32x4=True), g.a(vel3, RW, f32x4=True), g.a(pos4, W, f32x4=True)], jacc.jacc_nbody_params_t(1 << 14, 0.016, 0.01, 1.0))
 g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img3, R), g.a(f, R), g.a(out3, W)], jacc.jacc_conv2d_params_t(4736, 4096, 2, 0))
+# round 2: the pre-split SGEMM fallback (K = 101: lda not a multiple of 4; the
+# default 16-byte-aligned shapes above take the CTA-pair kernel), the halo
+# exchange + halo-row convolution (TMA and simple kernels), an RW histogram
+A3, B3 = synth.sgemm_inputs(130, 260, 101, "signed"); C3 = np.zeros((130, 260), np.float32)
+g.add_task(J.JACC_OP_SGEMM_F32, [g.a(A3, R), g.a(B3, R), g.a(C3, W)], jacc.jacc_sgemm_params_t(130, 260, 101, 101, 260, 260, 0, 0))
+for (hh, ww) in ((70, 132), (45, 77)):
+    band = synth.uniform_f32(hh * ww, 7).reshape(hh, ww); ext = np.zeros((hh + 4, ww), np.float32); ob = np.zeros_like(band)
+    g.add_task(J.JACC_OP_HALO_EXCHANGE_F32, [g.a(band, R), g.a(ext, W)], jacc.jacc_halo_params_t(hh, ww, 2, 0))
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(ext, R), g.a(f, R), g.a(ob, W)], jacc.jacc_conv2d_params_t(hh, ww, 2, J.JACC_CONV2D_HALO_ROWS))
+bins_rw = np.ones(256, np.int32)
+g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins_rw, RW)], jacc.jacc_hist_params_t(256))
 g.run(); g.run()
 print("ok", g.stats()["launches"])
 g.destroy()

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-flush", action="store_true", help="no L2 flush between reps (warm L2 / back-to-back)")
     ap.add_argument("--mode", default="3xtf32")
+    ap.add_argument("--m", type=int, default=0, help="sgemm: rows of A / C (default n; a 1/8 row block = 1024)")
     ap.add_argument("--shards", type=int, default=1, help="nbody: time rank 0's target shard of N/shards bodies")
     ap.add_argument("--p2p", action="store_true",
                     help="hist/reduce/nbody: follow the op with its collective (allreduce / allgather) in a "
@@ -75,11 +76,12 @@ def main():
             units, kind = 12 * n, "GB/s"
         elif op == "sgemm":
             n = a.n or synth.CFG4_MNK
-            A, B = synth.sgemm_inputs(n, n, n)
+            m = a.m or n
+            A, B = synth.sgemm_inputs(m, n, n)
             mode = J.JACC_SGEMM_3XTF32 if a.mode == "3xtf32" else J.JACC_SGEMM_FFMA
-            g.add_task(J.JACC_OP_SGEMM_F32, [g.a(D(A), R), g.a(D(B), R), g.a(D(np.zeros((n, n), np.float32)), W)],
-                       jacc.jacc_sgemm_params_t(n, n, n, n, n, n, mode, 0))
-            units, kind = 2 * n ** 3, "TFLOP/s"
+            g.add_task(J.JACC_OP_SGEMM_F32, [g.a(D(A), R), g.a(D(B), R), g.a(D(np.zeros((m, n), np.float32)), W)],
+                       jacc.jacc_sgemm_params_t(m, n, n, n, n, n, mode, 0))
+            units, kind = 2 * m * n * n, "TFLOP/s"
         elif op == "nbody":
             n = a.n or synth.CFG5_N
             pos, vel = synth.nbody_state(n)

@@ -14,9 +14,10 @@ import json
 import sys
 from collections import defaultdict
 
-TASK_OF = [("vadd_v4_kernel", "vadd"), ("reduce_kernel", "reduce"), ("hist256_kernel", "hist"),
-           ("bs_v4_kernel", "bs"), ("split_a_kernel", "sgemm"), ("split_bt_kernel", "sgemm"),
-           ("gemm_3xtf32_kernel", "sgemm"), ("nbody_partial_kernel", "nbody"), ("nbody_finish_kernel", "nbody")]
+TASK_OF = [("vadd_v4_kernel", "vadd"), ("jacc_k::<unnamed>::reduce_kernel", "reduce"), ("hist256", "hist"),
+           ("bs_v4_kernel", "bs"), ("gemm_3xtf32_pair_kernel", "sgemm"), ("split_a_kernel", "sgemm"),
+           ("split_bt_kernel", "sgemm"), ("gemm_3xtf32_kernel", "sgemm"), ("nbody_partial", "nbody"),
+           ("nbody_finish_kernel", "nbody")]
 INSTANCES = {"nbody": ("nbody_partial_kernel",)}   # count tasks by their first kernel
 
 
