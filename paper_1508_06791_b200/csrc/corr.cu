@@ -290,6 +290,192 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------- CTA pair
+// The same GEMM on 256 x 256 output tiles computed by a CTA PAIR
+// (tcgen05.mma.cta_group::2.kind::i8, M = 256, N = 256, K = 32): CTA x of the
+// pair stages A rows [128 x, 128 x + 128) and B rows (output columns)
+// [128 x, 128 x + 128) of the tile, the leader's single thread issues the
+// MMAs, which read both CTAs' shared memory and leave output rows
+// [128 x, ...) in CTA x's TMEM.  Per SM and 128-byte K block the operands
+// are 32 KB instead of 48 KB: the 1-SM kernel was bound by that ingest
+// (655 cycles per K block, ~75 B/clk/SM).  Both CTAs' TMA loads complete on
+// the LEADER's full barrier (cta_group::2 TMA, mbarrier in the peer CTA);
+// the MMA commits arrive on both CTAs' empty barriers (multicast).
+// Split-K: a (2, 1, S) cluster, rank = x + 2 z; CTA (x, z) adds rows
+// [r0, r1) of the S partials with the same x over DSMEM, in split order.
+constexpr int kHalfN = BN / 2;
+constexpr int kStage2 = BM * BK + kHalfN * BK;   // 32 KB
+constexpr int kStages2 = 6;
+constexpr int kSmem2 = kStages2 * kStage2 + 1024 + 256;
+static_assert(BM * kTileStride * 4 <= kStages2 * kStage2, "partial tile fits in the ring");
+constexpr uint32_t kIdesc2 = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc2), "r"(accum));
+}
+// arrive on the barrier at `bar` in both CTAs of the pair (cluster ranks
+// leader, leader + 1) once the MMAs issued so far have completed
+__device__ __forceinline__ void commit_pair(uint32_t bar, uint32_t leader) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"((uint16_t)(3u << leader))
+        : "memory");
+}
+// 2-D TMA whose completion is counted on the pair leader's mbarrier (cluster
+// rank `leader`: with a (2, 1, S) cluster the pairs are ranks 2z, 2z + 1)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar,
+                                                 uint32_t leader) {
+    uint32_t lb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(lb) : "r"(bar), "r"(leader));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(lb)
+        : "memory");
+}
+
+template <int S>
+__device__ __forceinline__ void cluster_sum_pair(uint32_t tile, int r0, int r1, int x, int m_blk2, int n_blk, int32_t *C,
+                                                 int64_t ta, int64_t tb, bool vec) {
+    constexpr int kU = S <= 4 ? 4 : 2;
+    const int nitems = (r1 - r0) * (BN / 4);
+    for (int it0 = threadIdx.x; it0 < nitems; it0 += kU * kThreads) {
+        int4 v[kU][S];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            const uint32_t off = (uint32_t)((r0 + it / (BN / 4)) * kTileStride + (it % (BN / 4)) * 4) * 4;
+#pragma unroll
+            for (int sp = 0; sp < S; ++sp)
+                if (it < nitems) v[u][sp] = ld_dsmem_v4(tile + off, (uint32_t)(x + 2 * sp));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            if (it >= nitems) continue;
+            int4 acc = v[u][0];
+#pragma unroll
+            for (int sp = 1; sp < S; ++sp) {
+                acc.x += v[u][sp].x; acc.y += v[u][sp].y; acc.z += v[u][sp].z; acc.w += v[u][sp].w;
+            }
+            const int lr = r0 + it / (BN / 4), lc = (it % (BN / 4)) * 4;
+            const int64_t row = (int64_t)m_blk2 * 2 * BM + x * BM + lr, col = (int64_t)n_blk * BN + lc;
+            if (row >= ta || col >= tb) continue;
+            int32_t *c = C + row * tb + col;
+            if (vec) {
+                *(int4 *)c = acc;
+            } else {
+                const int32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+                for (int k = 0; k < 4 && col + k < tb; ++k) c[k] = a4[k];
+            }
+        }
+    }
+}
+
+// grid (2 * tbp / BN, tap / (2 BM), S); cluster (2, 1, S)
+__global__ void __launch_bounds__(kThreads, 1)
+    corr_i8_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                        int32_t *__restrict__ C, int64_t ta, int64_t tb, int num_kb) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *bars = (uint64_t *)(smem + kStages2 * kStage2);
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages2 + 1);
+    const uint32_t full0 = tc::smem_u32(bars), empty0 = tc::smem_u32(bars + kStages2),
+                   tfull = tc::smem_u32(bars + 2 * kStages2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = (int)(blockIdx.x & 1);           // rank in the pair (cluster x)
+    const uint32_t leader = cluster_rank() & ~1u;  // the pair's even cluster rank (= 2 z)
+    const int n_blk = blockIdx.x >> 1, m_blk2 = blockIdx.y;
+    const int S = (int)gridDim.z;
+    const int per = (num_kb + S - 1) / S;
+    const int kb0 = blockIdx.z * per, kb1 = min(num_kb, kb0 + per);
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&map_a);
+        tc::tma_prefetch(&map_b);
+        for (int s = 0; s < kStages2; ++s) {
+            tc::mbar_init(full0 + 8 * s, 1);
+            tc::mbar_init(empty0 + 8 * s, 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc::fence_before();
+    cluster_sync();    // barriers of every CTA initialised before any remote arrive / complete_tx
+    tc::fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {   // TMA producer (each CTA): its A rows and its B rows, counted on the leader's barrier
+            asm volatile("griddepcontrol.wait;" ::: "memory");   // the unpack grid has completed
+            for (int i = 0; i < kb1 - kb0; ++i) {
+                const int s = i % kStages2, kb = kb0 + i;
+                tc::mbar_wait(empty0 + 8 * s, ((i / kStages2) & 1) ^ 1);
+                uint8_t *st = smem + s * kStage2;
+                if (x == 0) tc::mbar_expect_tx(full0 + 8 * s, 2 * kStage2);
+                tma_load_2d_pair(tc::smem_u32(st), &map_a, kb * BK, m_blk2 * 2 * BM + x * BM, full0 + 8 * s,
+                                 leader);
+                tma_load_2d_pair(tc::smem_u32(st + BM * BK), &map_b, kb * BK, n_blk * BN + x * kHalfN,
+                                 full0 + 8 * s, leader);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && x == 0) {   // MMA issuer: the leader's single thread
+            for (int i = 0; i < kb1 - kb0; ++i) {
+                const int s = i % kStages2;
+                tc::mbar_wait(full0 + 8 * s, (i / kStages2) & 1);
+                tc::fence_after();
+                const uint32_t a = tc::smem_u32(smem + s * kStage2), b = a + BM * BK;
+#pragma unroll
+                for (int k = 0; k < BK / 32; ++k)
+                    mma_i8_pair(tmem_d, tc::desc_kmajor(a + 32 * k, 128), tc::desc_kmajor(b + 32 * k, 128),
+                                (i | k) != 0);
+                commit_pair(empty0 + 8 * s, leader);
+            }
+            commit_pair(tfull, leader);
+        }
+    } else {   // epilogue warps 2..5: TMEM lane quarter -> this CTA's partial tile in its drained ring
+        const int q = warp & 3;
+        tc::mbar_wait(tfull, 0);
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            JACC_TMEM_LD_32(tmem_d + ((uint32_t)(q * 32) << 16) + c * 32, r);
+            tc::wait_ld();
+            int32_t *trow = (int32_t *)smem + (q * 32 + lane) * kTileStride + c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *(int4 *)(trow + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
+        }
+    }
+    tc::fence_before();
+    cluster_sync();    // every CTA's partial tile is in its shared memory; all MMAs have completed
+    if (warp == 1) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(kTmemCols));
+    }
+    const int z = (int)blockIdx.z;
+    const int r0 = z * BM / S, r1 = (z + 1) * BM / S;
+    const uint32_t tile = tc::smem_u32(smem);
+    const bool vec = (tb & 3) == 0 && (((uintptr_t)C) & 15) == 0;
+    switch (S) {
+        case 1: cluster_sum_pair<1>(tile, r0, r1, x, m_blk2, n_blk, C, ta, tb, vec); break;
+        case 2: cluster_sum_pair<2>(tile, r0, r1, x, m_blk2, n_blk, C, ta, tb, vec); break;
+        case 3: cluster_sum_pair<3>(tile, r0, r1, x, m_blk2, n_blk, C, ta, tb, vec); break;
+        default: cluster_sum_pair<4>(tile, r0, r1, x, m_blk2, n_blk, C, ta, tb, vec); break;
+    }
+    cluster_sync_relaxed();   // no CTA leaves while a peer still reads its tile
+}
+
 // C[i][j] = sum over splits of the partial tiles, in split order (exact).
 // One row per blockIdx.y; 16-byte loads of the padded partials.
 __global__ void __launch_bounds__(256) split_sum_kernel(const int32_t *__restrict__ part, int splits, int64_t tap,
@@ -356,7 +542,52 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
     if (!tc::make_map_2d(&ma, xa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tap, kp, kp, BM, BK, 128) ||
         !tc::make_map_2d(&mb, xb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tbp, kp, kp, BN, BK, 128))
         return cudaErrorInvalidValue;
-    cudaError_t e = set_max_dyn_smem((const void *)corr_i8_kernel, kSmemBytes);
+    cudaError_t e;
+    {   // CTA pairs on 256 x 256 tiles, split-K in a (2, 1, S <= 4) cluster; A rows
+        // past the unpacked tap come from TMA's zero fill
+        const int64_t tap2 = round_up(ta, 2 * BM), num_kb = kp / BK;
+        const int64_t pairs = (tap2 / (2 * BM)) * (tbp / BN);
+        int64_t S = sm_count() / (2 * pairs);
+        if (S > num_kb / 8) S = num_kb / 8;
+        S = S < 1 ? 1 : S > 4 ? 4 : S;
+        // Only when the pairs fill at least half the SMs with <= 2 splits:
+        // with fewer tiles the split-K clusters of 8 CTAs (2 x 4) are not all
+        // co-resident (measured 1024 x 131072: 188 us vs 128 for the 1-SM
+        // kernel's (1, 1, 4) clusters); those shapes keep the 1-SM kernel.
+        const bool use_pair = 2 * pairs * (S < 2 ? S : 2) >= sm_count() / 2;
+        if (S > 2) S = 2;
+        CUtensorMap pa, pb;
+        if (use_pair &&
+            tc::make_map_2d(&pa, xa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, same ? tbp : tap, kp, kp, BM, BK, 128) &&
+            tc::make_map_2d(&pb, xb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, tbp, kp, kp, kHalfN, BK, 128) &&
+            tap2 / (2 * BM) <= 65535) {
+            e = set_max_dyn_smem((const void *)corr_i8_pair_kernel, kSmem2);
+            if (e != cudaSuccess) return e;
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = (unsigned)S;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.gridDim = dim3((unsigned)(2 * (tbp / BN)), (unsigned)(tap2 / (2 * BM)), (unsigned)S);
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = kSmem2;
+            cfg.stream = st;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (max_active_clusters((const void *)corr_i8_pair_kernel, &cfg) >= (S > 1 ? pairs : 1)) {
+                cfg.numAttrs = 2;
+                e = cudaLaunchKernelEx(&cfg, corr_i8_pair_kernel, (CUtensorMap)pa, (CUtensorMap)pb, C, ta, tb,
+                                       (int)num_kb);
+                ++*launches;
+                if (e != cudaSuccess) return e;
+                return cudaGetLastError();
+            }
+        }
+    }
+    e = set_max_dyn_smem((const void *)corr_i8_kernel, kSmemBytes);
     if (e != cudaSuccess) return e;
     const int splits = corr_splits(ta, tb, words);
     dim3 grid((unsigned)(tbp / BN), (unsigned)(tap / BM), (unsigned)splits);
