@@ -778,6 +778,62 @@ def hist_kiter_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev, K=400):
             "bins_correct_rank0": ok, "collectives": "p2p (fused into the histogram)" if p2p else "nccl"}
 
 
+def conv2d_bands_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev, n=16384, reps=5):
+    """SURVEY §8(f) f1 at N > 1: the 16384^2 5x5 convolution sharded by row
+    bands -- each rank holds its band (DEVICE), exchanges the 2 halo rows with
+    its neighbours (JACC_OP_HALO_EXCHANGE_F32) and convolves its extended
+    band (JACC_CONV2D_HALO_ROWS).  Device time per graph, max over ranks; L2
+    flushed before each rep; output rows checked against the one-GPU rows
+    of the same kernel is the GPU tests' job (tests/test_gpu_p2p.py)."""
+    from paper_1508_06791_b200 import jacc
+    from paper_1508_06791_b200.torch_glue import make_graph, peer_setup
+    R_, W_ = J.JACC_READ, J.JACC_WRITE
+    dev = torch.device("cuda", torch.cuda.current_device())
+    flags = J.JACC_GRAPH_REPLAY | J.JACC_GRAPH_NO_TIMING | J.JACC_GRAPH_SERIAL | (J.JACC_GRAPH_P2P if p2p else 0)
+    g, st = make_graph(dev.index, n_streams=1, rank=rank, world=world, nccl_comm=0 if p2p else comm_ptr,
+                       flags=flags)
+    if p2p:
+        peer_setup(g, 4 << 20)
+    lo, hi = synth.shard_range(n, rank, world)
+    r = 2
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    img = torch.rand((n, n), device=dev, generator=gen) * 2 - 1
+    band = img[lo:hi].contiguous()
+    del img
+    ext = torch.empty((hi - lo + 2 * r, n), device=dev)
+    out = torch.empty((hi - lo, n), device=dev)
+    f = torch.from_numpy(synth.uniform_f32(25, 12, -1, 1).reshape(5, 5)).to(dev)
+    g.add_task(J.JACC_OP_HALO_EXCHANGE_F32, [g.a(band, R_), g.a(ext, W_)], jacc.jacc_halo_params_t(hi - lo, n, r, 0))
+    g.add_task(J.JACC_OP_CONV2D_F32, [g.a(ext, R_), g.a(f, R_), g.a(out, W_)],
+               jacc.jacc_conv2d_params_t(hi - lo, n, r, J.JACC_CONV2D_HALO_ROWS))
+    g.run()   # capture
+    flush = L2Flush(torch, dev)
+    comp = st["compute"][0]
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        g.execute()
+        e1.record(comp)
+        g.sync()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    g.destroy()
+    del band, ext, out, flush
+    torch.cuda.empty_cache()
+    nbytes = 8 * n * n   # the whole image read + written, over all ranks
+    return {"n": n, "ranks": world, "ms_per_graph": float(t.item()),
+            "achieved_GBps_all_ranks": nbytes / (float(t.item()) * 1e-3) / 1e9,
+            "collectives": "p2p halo exchange" if p2p else "nccl send/recv halo exchange",
+            "note": "halo exchange + halo-row convolution per rank, device time, max over ranks"}
+
+
 _BINS_REF = None
 
 
@@ -1037,11 +1093,16 @@ def run_jacc(args):
                   "note": "the N-body step's bound is its FP32 compute; the all-gather's NVLink time per step is "
                           "this share of it and overlaps the kick/drift stores"}
     hist_kiter = None
+    conv_bands = None
     if world > 1:
         try:
             hist_kiter = hist_kiter_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev)
         except Exception as exc:
             hist_kiter = {"error": str(exc)[:300]}
+        try:
+            conv_bands = conv2d_bands_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev)
+        except Exception as exc:
+            conv_bands = {"error": str(exc)[:300]}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -1066,7 +1127,8 @@ def run_jacc(args):
                        "sgemm_mode": args.sgemm_mode},
             "nranks": len(ranks_seen), "ranks": ranks_seen,
             "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "clocks": clocks,
-            "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "nvlink": nvlink,
+            "e2e": e2e, "step_ms": times, "hist_kiter_spmd": hist_kiter, "conv2d_bands_spmd": conv_bands,
+            "nvlink": nvlink,
             "counted_copies_device_resident": {
                 "h2d": int(stats["h2d_count"]), "d2h": int(stats["d2h_count"])}}
     if world == 1 and not args.no_e2e:

@@ -60,3 +60,6 @@ def test_main_arm_two_ranks_without_torchrun():
     assert line["n_gpus"] == 2 and line["nranks"] == 2
     assert sorted(x["rank"] for x in line["ranks"]) == [0, 1]
     assert line["config"]["collectives"].startswith("p2p")
+    # the N > 1 extras ran: the paper's histogram protocol and the row-band convolution
+    assert "error" not in line["hist_kiter_spmd"] and line["hist_kiter_spmd"]["bins_correct_rank0"]
+    assert "error" not in line["conv2d_bands_spmd"], line["conv2d_bands_spmd"]
