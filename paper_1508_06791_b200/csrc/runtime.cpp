@@ -870,7 +870,7 @@ int launch_task(jacc_graph *g, Task &T, cudaStream_t st, int *launches, const Ta
             float *ext = (float *)P(1);
             const int rk = g->cfg.rank, wd = g->cfg.world;
             if (hp->rows * hp->W == 0 && wd == 1) break;
-            if (p2p(g) && wd > 1) {
+            if (p2p(g)) {   // peer-memory push + finish (at world 1: the same kernels, no neighbours)
                 e = jacc_k::peer_halo(peer_op(g, T), band, ext, hp->rows, hp->W, hp->radius, st, launches);
                 break;
             }

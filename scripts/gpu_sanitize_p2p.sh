@@ -28,6 +28,8 @@ g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins, W)], jacc.jacc_hist
 g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(bins, RW)])
 g.add_task(J.JACC_OP_ALLREDUCE_SUM, [g.a(big, RW)])
 g.add_task(J.JACC_OP_ALLGATHER, [g.a(pos, R, f32x4=True), g.a(ALL, W, f32x4=True)])
+band = synth.uniform_f32(70 * 132, 6).reshape(70, 132); ext = np.zeros((74, 132), np.float32)
+g.add_task(J.JACC_OP_HALO_EXCHANGE_F32, [g.a(band, R), g.a(ext, W)], jacc.jacc_halo_params_t(70, 132, 2, 0))
 g.add_task(J.JACC_OP_NBODY_STEP_F32, [g.a(ALL, R, f32x4=True), g.a(vel, RW, f32x4=True), g.a(pos2, W, f32x4=True)], jacc.jacc_nbody_params_t(0, 0.016, 0.01, 1.0))
 g.add_task(J.JACC_OP_ALLGATHER, [g.a(pos2, R, f32x4=True), g.a(ALL, W, f32x4=True)])
 g.add_task(J.JACC_OP_BROADCAST, [g.a(bc, RW)], jacc.jacc_bcast_params_t(0))

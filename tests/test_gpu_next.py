@@ -225,11 +225,14 @@ def test_conv2d_halo_rows_world1(shape, r):
     H, Wd = shape
     img = synth.uniform_f32(H * Wd, 700 + H, -1, 1).reshape(H, Wd)
     f = synth.uniform_f32((2 * r + 1) ** 2, 701, -1, 1).reshape(2 * r + 1, 2 * r + 1)
-    g, _ = make_graph(0)
-    ext, out = _conv_band_graph(g, img, f, H, Wd, r)
-    g.run()
-    g.destroy()
-    assert np.array_equal(ext, oracle.halo_band(img, 0, H, r))
+    for flags in (0, J.JACC_GRAPH_P2P):   # the local kernel; the peer push + finish kernels at world 1
+        g, _ = make_graph(0, flags=flags)
+        ext, out = _conv_band_graph(g, img, f, H, Wd, r)
+        for _ in range(3):                 # three epochs: both staging parities of the peer path
+            ext[:] = np.nan
+            g.run()
+            assert np.array_equal(ext, oracle.halo_band(img, 0, H, r)), flags
+        g.destroy()
     plain = np.zeros_like(img)
     g, _ = make_graph(0)
     g.add_task(J.JACC_OP_CONV2D_F32, [g.a(img, R), g.a(f, R), g.a(plain, W)], jacc.jacc_conv2d_params_t(H, Wd, r, 0))
