@@ -187,17 +187,25 @@ def test_hist_bit_exact(n, dist, nbins):
     g.destroy()
 
 
-@pytest.mark.parametrize("off", [1, 2, 3])
-def test_hist_unaligned_and_accumulate(off):
-    n = 300007
+@pytest.mark.parametrize("mode", ["RW", "W"])
+@pytest.mark.parametrize("off,n", [(1, 300007), (2, 300007), (3, 300007), (1, 3), (3, 6)])
+def test_hist_unaligned_and_accumulate(off, n, mode):
+    """Unaligned key views (head keys counted by the edge path into the
+    workspace accumulator before the main kernel), W (bins assigned by the
+    last block: no memset) and RW (host bins + counts), incl. views with
+    fewer than 4 aligned keys."""
     keys = synth.hist_keys(n + off, 256, seed=4)
     dk = _dev(keys)
     init = np.arange(256, dtype=np.int32)
     bins = init.copy()
     g = _graph()
-    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(dk[off:], R), g.a(bins, RW)], jacc.jacc_hist_params_t(256))
-    g.run()
-    assert np.array_equal(bins, oracle.histogram(keys[off:], 256, init=init))
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(dk[off:], R), g.a(bins, RW if mode == "RW" else W)],
+               jacc.jacc_hist_params_t(256))
+    for _ in range(2):   # the accumulator must be re-zeroed by the first launch
+        bins[:] = init
+        g.run()
+        want = oracle.histogram(keys[off:], 256, init=init if mode == "RW" else None)
+        assert np.array_equal(bins, want)
     g.destroy()
 
 
@@ -290,7 +298,10 @@ def _sgemm(A, B, mode, device_args=False):
     return out
 
 
-SG_SHAPES = [(1, 1, 1), (127, 129, 65), (256, 256, 256), (300, 520, 1000), (1024, 768, 2048)]
+# (1,1,1), (127,129,65): unaligned strides -> the pre-split path; the rest the
+# CTA-pair path, incl. tiles mostly outside M / N and a K tail inside a block
+SG_SHAPES = [(1, 1, 1), (127, 129, 65), (8, 16, 32), (200, 40, 20), (64, 300, 48), (256, 256, 256),
+             (300, 520, 1000), (1024, 768, 2048)]
 
 
 @pytest.mark.parametrize("mode", [J.JACC_SGEMM_FFMA, J.JACC_SGEMM_3XTF32], ids=["ffma", "3xtf32"])
