@@ -541,6 +541,14 @@ def roofline_points(torch, J, peaks, reps=10):
         torch.cuda.empty_cache()
     del flush
     torch.cuda.empty_cache()
+    try:   # the ncu kernel time of the same launch, beside the event times (profiles/)
+        nk = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernel_us.json")))
+        for k, v in out.items():
+            if k in nk:
+                v["ncu_kernel_us"] = nk[k]
+                v["ncu_frac"] = v["bytes_per_launch"] / (nk[k] * 1e-6) / 1e9 / peaks["hbm_gbs"]
+    except Exception:
+        pass
     return out
 
 

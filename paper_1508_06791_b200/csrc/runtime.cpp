@@ -25,6 +25,8 @@
 #include "kernels.h"
 #include "nccl_dl.h"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges show in nsys / ncu when a tool is attached
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -1329,7 +1331,14 @@ static double now_us() {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// NVTX range for the scope of an ABI call (a no-op unless a tool injects NVTX)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 int jacc_graph_execute(jacc_graph_t *g) {
+    NvtxRange nvtx("jacc_graph_execute");
     if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
     if (g->state == ST_EXECUTING) return fail(JACC_ERR_STATE, "graph is already executing");
     const double t0 = log_on() ? now_us() : 0.0;
@@ -1367,6 +1376,7 @@ int jacc_graph_execute(jacc_graph_t *g) {
 }
 
 int jacc_graph_sync(jacc_graph_t *g) {
+    NvtxRange nvtx("jacc_graph_sync");
     if (!g) return fail(JACC_ERR_INVALID_ARG, "NULL graph");
     if (g->state != ST_EXECUTING) {
         if (g->state == ST_FAILED) return g->pending_error ? g->pending_error : JACC_ERR_STATE;
