@@ -333,6 +333,16 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
     traffic = _traffic()
     for name in out:
         out[name]["traffic"] = traffic.get(name)
+    # the memory roof of each HBM task's own read/write mix (scripts/micro/stream_mix.cu, profiles/)
+    try:
+        mix = json.load(open(os.path.join(ROOT, "profiles", "stream_mix.json")))
+        for name, key in (("bs", "read1_write2"), ("hist", "read_only"), ("vadd", "read2_write1"),
+                          ("reduce", "read_only")):
+            if name in out and "achieved" in out[name]:
+                out[name]["mix_stream_GBps"] = mix[key]
+                out[name]["frac_of_mix_stream"] = out[name]["achieved"] / mix[key]
+    except Exception:
+        pass
     return out
 
 
