@@ -343,6 +343,20 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
                 out[name]["frac_of_mix_stream"] = out[name]["achieved"] / mix[key]
     except Exception:
         pass
+    # N-body against the measured paired-FP32 ceiling (scripts/micro/fp32_pipes.cu, profiles/): 11 paired
+    # lane-ops per interaction (equal-mass tiles) per clock per SM
+    try:
+        pipes = json.load(open(os.path.join(ROOT, "profiles", "fp32_pipes.json")))
+        nb = out.get("nbody")
+        if nb and "achieved" in nb:
+            ceiling = max(pipes["ffma2"].values())
+            lane_ops = nb["flop_per_launch"] / 20.0 * 11.0
+            per_clk = lane_ops / (nb["ms"] * 1e-3) / (peaks["sm_max_mhz"] * 1e6) / 148
+            nb["lane_ops_per_clk_sm"] = per_clk
+            nb["measured_pipe_ceiling"] = ceiling
+            nb["frac_of_measured_pipe"] = per_clk / ceiling
+    except Exception:
+        pass
     return out
 
 
