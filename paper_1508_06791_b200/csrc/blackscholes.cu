@@ -188,6 +188,57 @@ __global__ void __launch_bounds__(256, kMinBlocks) bs_v4_kernel(const float4 *__
     if (t < tail) bs_aparapi(ut[t], ct[t], pt[t]);
 }
 
+// 256-bit I/O (sm_100 LDG.256 / STG.256): 8 options per thread per trip, the
+// next trip's vector loaded before this one is priced.  Measured at 2^26
+// (same-box A/B, scripts/ab/ab.sh): 137.3 us vs 141.4 us for the 128-bit
+// kernel above at its best depth; the plain 1-read : 2-write stream of
+// scripts/micro/stream_shape.cu peaks with this shape too (256-bit, one
+// vector per thread in flight: 130 us = 6.18 TB/s, vs 5.80 TB/s for 128-bit
+// accesses three deep).  Default (write-back) stores: .cs measured the same.
+struct f8 {
+    float v[8];
+};
+__device__ __forceinline__ f8 ld_stream8(const float *p) {
+    f8 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st8(float *p, const f8 &r) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]),
+                 "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256, 4) bs_v8_kernel(const float *__restrict__ u, float *__restrict__ call,
+                                                       float *__restrict__ put, int64_t n8, const float *__restrict__ ut,
+                                                       float *__restrict__ ct, float *__restrict__ pt, int tail) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    f8 nxt;
+    if (i < n8) nxt = ld_stream8(u + 8 * i);
+    for (; i < n8; i += stride) {
+        const f8 cur = nxt;
+        if (i + stride < n8) nxt = ld_stream8(u + 8 * (i + stride));
+        f8 c, p;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            float2 cc, pp;
+            bs_aparapi2(make_float2(cur.v[2 * h], cur.v[2 * h + 1]), cc, pp);
+            c.v[2 * h] = cc.x;
+            c.v[2 * h + 1] = cc.y;
+            p.v[2 * h] = pp.x;
+            p.v[2 * h + 1] = pp.y;
+        }
+        st8(call + 8 * i, c);
+        st8(put + 8 * i, p);
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tail) bs_aparapi(ut[t], ct[t], pt[t]);
+}
+
 __global__ void __launch_bounds__(256) bs_scalar_kernel(const float *__restrict__ u, float *__restrict__ call,
                                                         float *__restrict__ put, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -210,7 +261,12 @@ cudaError_t blackscholes_f32(const float *u, float *call, float *put, int64_t n,
                              cudaStream_t st, int *launches) {
     if (n <= 0) return cudaSuccess;
     int grid, block;
-    if (aligned16(u) && aligned16(call) && aligned16(put)) {
+    if ((((uintptr_t)u | (uintptr_t)call | (uintptr_t)put) & 31) == 0) {   // 256-bit accesses
+        const int64_t n8 = n / 8;
+        pick_grid(s, (n8 + 255) / 256, 8, 256, &grid, &block);
+        bs_v8_kernel<<<grid, block, 0, st>>>(u, call, put, n8, u + 8 * n8, call + 8 * n8, put + 8 * n8,
+                                             (int)(n - 8 * n8));
+    } else if (aligned16(u) && aligned16(call) && aligned16(put)) {
         const int64_t n4 = n / 4;
         // (A TMA-staged variant -- cp.async.bulk into a 4-stage mbarrier ring,
         // 8 consumer warps -- measured 163 us vs 155 us for this one: the

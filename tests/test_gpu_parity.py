@@ -246,6 +246,29 @@ def test_bs_aparapi(n):
     g.destroy()
 
 
+@pytest.mark.parametrize("off", [0, 4, 2, 1])
+def test_bs_alignment_paths(off):
+    """The three kernels of the APARAPI map: 256-bit I/O (32-byte aligned
+    views), 128-bit (16-byte aligned), scalar (any) -- every one within the
+    R12 gate of the oracle, tails included."""
+    n = 20011
+    u = synth.bs_rand(n, seed=77)
+    base = torch.zeros(n + 8, device="cuda")
+    du = base[off:off + n]
+    du.copy_(torch.from_numpy(u))
+    cbase = torch.zeros(n + 8, device="cuda"); pbase = torch.zeros(n + 8, device="cuda")
+    dc, dp = cbase[off:off + n], pbase[off:off + n]
+    g = _graph()
+    g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(du, R), g.a(dc, W), g.a(dp, W)])
+    g.run()
+    oc, op = oracle.blackscholes(u)
+    uu = u.astype(np.float64)
+    S = 10 * uu + 100 * (1 - uu); T = uu + 10 * (1 - uu); Rr = 0.01 * uu + 0.05 * (1 - uu)
+    _bs_gate(dc.cpu().numpy(), dp.cpu().numpy(), oc, op, S + S * np.exp(-Rr * T))
+    assert float(cbase[:off].abs().sum()) == 0 and float(cbase[off + n:].abs().sum()) == 0
+    g.destroy()
+
+
 def test_bs_full_size_config3_sampled():
     u = synth.bs_rand()
     du = _dev(u)
