@@ -175,10 +175,61 @@ __device__ __forceinline__ void cluster_sum(uint32_t tile, int r0, int r1, int m
     }
 }
 
+// The same with 16-bit partials (each split's count is <= its K bits, so
+// u16 holds it when a split spans <= 511 K blocks of 128): the partial rows
+// are 256 u16 = 128 words, padded to kTileStride16; an item is 8 columns
+// (one 16-byte DSMEM load per split) -- half the remote bytes of the 32-bit
+// form, whose ~4.6 us of latency-bound DSMEM reads dominated the split-K
+// epilogue at the paper's size.
+constexpr int kTileStride16 = BN / 2 + 4;   // words per u16 partial row
+template <int S>
+__device__ __forceinline__ void cluster_sum16(uint32_t tile, int r0, int r1, int m_blk, int n_blk, int32_t *C,
+                                              int64_t ta, int64_t tb, bool vec) {
+    constexpr int kU = S <= 4 ? 4 : 2;
+    const int nitems = (r1 - r0) * (BN / 8);
+    for (int it0 = threadIdx.x; it0 < nitems; it0 += kU * kThreads) {
+        int4 v[kU][S];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            const uint32_t off = (uint32_t)((r0 + it / (BN / 8)) * kTileStride16 + (it % (BN / 8)) * 4) * 4;
+#pragma unroll
+            for (int sp = 0; sp < S; ++sp)
+                if (it < nitems) v[u][sp] = ld_dsmem_v4(tile + off, (uint32_t)sp);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int it = it0 + u * kThreads;
+            if (it >= nitems) continue;
+            int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int sp = 0; sp < S; ++sp) {
+                const uint32_t w[4] = {(uint32_t)v[u][sp].x, (uint32_t)v[u][sp].y, (uint32_t)v[u][sp].z,
+                                       (uint32_t)v[u][sp].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    acc[2 * h] += (int)(w[h] & 0xFFFFu);
+                    acc[2 * h + 1] += (int)(w[h] >> 16);
+                }
+            }
+            const int lr = r0 + it / (BN / 8), lc = (it % (BN / 8)) * 8;
+            const int64_t row = (int64_t)m_blk * BM + lr, col = (int64_t)n_blk * BN + lc;
+            if (row >= ta || col >= tb) continue;
+            int32_t *c = C + row * tb + col;
+            if (vec && col + 8 <= tb) {
+                *(int4 *)c = make_int4(acc[0], acc[1], acc[2], acc[3]);
+                *(int4 *)(c + 4) = make_int4(acc[4], acc[5], acc[6], acc[7]);
+            } else {
+                for (int k = 0; k < 8 && col + k < tb; ++k) c[k] = acc[k];
+            }
+        }
+    }
+}
+
 // C tile (m_blk, n_blk) over K blocks [kb0, kb1).  ldc = tb and bounds
 // checks when writing C directly; a padded [tap x tbp] partial (split
 // blockIdx.z) when `part` is set; summed over the cluster's DSMEM when
-// `csum` is set (cluster dims (1, 1, gridDim.z)).
+// `csum` is set (cluster dims (1, 1, gridDim.z); 2: 16-bit partials).
 __global__ void __launch_bounds__(kThreads, 1)
     corr_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    int32_t *__restrict__ C, int64_t ta, int64_t tb, int num_kb, int32_t *__restrict__ part,
@@ -249,7 +300,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             JACC_TMEM_LD_32(tmem_d + ((uint32_t)(q * 32) << 16) + c * 32, r);
             tc::wait_ld();
             const int64_t col0 = (int64_t)n_blk * BN + c * 32;
-            if (csum) {   // partial tile into this CTA's drained ring memory
+            if (csum == 2) {   // u16 partial tile (per-split counts < 2^16) into the drained ring
+                uint32_t *trow = (uint32_t *)smem + (q * 32 + lane) * kTileStride16 + c * 16;
+#pragma unroll
+                for (int j = 0; j < 32; j += 8)
+                    *(uint4 *)(trow + j / 2) = make_uint4(r[j] | (r[j + 1] << 16), r[j + 2] | (r[j + 3] << 16),
+                                                          r[j + 4] | (r[j + 5] << 16), r[j + 6] | (r[j + 7] << 16));
+            } else if (csum) {   // partial tile into this CTA's drained ring memory
                 int32_t *trow = (int32_t *)smem + (q * 32 + lane) * kTileStride + c * 32;
 #pragma unroll
                 for (int j = 0; j < 32; j += 4)
@@ -277,7 +334,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r0 = rank * BM / S, r1 = (rank + 1) * BM / S;
         const uint32_t tile = tc::smem_u32(smem);
         const bool vec = (tb & 3) == 0 && (((uintptr_t)C) & 15) == 0;
-        switch (S) {   // the split count as a constant: every load of a pass in flight at once
+        if (csum == 2) {
+            switch (S) {
+                case 2: cluster_sum16<2>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                case 3: cluster_sum16<3>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                case 4: cluster_sum16<4>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                case 5: cluster_sum16<5>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                case 6: cluster_sum16<6>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                case 7: cluster_sum16<7>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+                default: cluster_sum16<8>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
+            }
+        } else switch (S) {   // the split count as a constant: every load of a pass in flight at once
             case 2: cluster_sum<2>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
             case 3: cluster_sum<3>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
             case 4: cluster_sum<4>(tile, r0, r1, m_blk, n_blk, C, ta, tb, vec); break;
@@ -608,8 +675,10 @@ cudaError_t corr_popc_u32(const uint32_t *A, int64_t ta, const uint32_t *B, int6
         cfg.numAttrs = 1;   // the occupancy query takes the cluster shape only
         if (max_active_clusters((const void *)corr_i8_kernel, &cfg) > 0) {   // cached per shape
             cfg.numAttrs = 2;
+            // 16-bit partials when every split's count fits (<= 511 K blocks of 128 bits per split)
+            const int per = (int)((kp / BK + splits - 1) / splits);
             e = cudaLaunchKernelEx(&cfg, corr_i8_kernel, (CUtensorMap)ma, (CUtensorMap)mb, C, ta, tb, (int)(kp / BK),
-                                   (int32_t *)nullptr, tap, tbp, 1);
+                                   (int32_t *)nullptr, tap, tbp, per * BK <= 65535 ? 2 : 1);
             ++*launches;
             if (e != cudaSuccess) return e;
             return cudaGetLastError();

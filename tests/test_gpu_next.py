@@ -63,13 +63,14 @@ def test_conv2d_tolerance(H, Wd, r):
     assert np.all(np.abs(out - ref) <= 1e-5 * ab + 1e-30)
 
 
-# split-K counts of the 1-SM kernel (pushed split slots, corr.cu): 1024^2 x 16384
+# split-K counts of the 1-SM kernel (split-K summed over DSMEM, corr.cu): 1024^2 x 16384
 # -> 4; (100, 70, 131072) -> 8 on one ragged tile; (1152, 768) -> 5; (1408,
-# 512) -> 6; (1280, 512) -> 7; (2000, 260) -> 4 with ragged rows and columns
+# 512) -> 6; (1280, 512) -> 7; (2000, 260) -> 4 with ragged rows and columns;
+# 16-bit split partials up to 511 K blocks per split, 32-bit beyond ((100, 70, 2^20): 1024)
 @pytest.mark.parametrize("ta,tb,docs", [(1, 1, 32), (5, 7, 96), (100, 70, 1000 * 32 // 32 * 32),
                                         (1024, 1024, 16384), (100, 70, 131072), (1152, 768, 8192),
                                         (1408, 512, 8192), (1280, 512, 8192), (2000, 260, 8192),
-                                        (700, 500, 4096)])
+                                        (700, 500, 4096), (100, 70, 1 << 20)])
 def test_corr_bit_exact(ta, tb, docs):
     A = synth.corr_bitsets(ta, docs, 0.5, seed=ta)
     B = synth.corr_bitsets(tb, docs, 0.3, seed=tb + 1)

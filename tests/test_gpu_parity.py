@@ -79,6 +79,32 @@ def test_vadd_ieee_specials_bit_exact():
     assert np.any((c != 0) & (np.abs(c) < 1.17549435e-38))                      # denormal results kept
 
 
+@pytest.mark.parametrize("off", [0, 4])
+def test_vadd_256bit_path_bit_exact(off):
+    """n >= 2^26: 32-byte aligned operands take the 256-bit kernel (off 0),
+    16-byte aligned views the 128-bit one (off 4); random values with IEEE
+    specials sprinkled in and a ragged tail of 13 -- bit-exact either way."""
+    n = (1 << 26) + 13
+    a, b = synth.vadd_inputs(n, seed=91)
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, 3.4028235e38, -3.4028235e38], np.float32)
+    idx = synth.rng(92).integers(0, n, 4096)
+    a[idx] = np.resize(sp, idx.size); b[idx[::-1]] = np.resize(sp, idx.size)
+    a[-13:] = sp[:8].tolist() + [1.0] * 5
+    da = torch.zeros(n + off, device="cuda"); db = torch.zeros(n + off, device="cuda")
+    dc = torch.zeros(n + off, device="cuda")
+    da[off:].copy_(torch.from_numpy(a)); db[off:].copy_(torch.from_numpy(b))
+    g = _graph()
+    g.add_task(J.JACC_OP_VADD_F32, [g.a(da[off:], R), g.a(db[off:], R), g.a(dc[off:], W)])
+    g.run()
+    g.destroy()
+    c = dc[off:].cpu().numpy()
+    ref = oracle.vadd(a, b)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(c), nan)
+    assert np.array_equal(c[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+    assert float(dc[:off].abs().sum()) == 0
+
+
 @pytest.mark.parametrize("off", [1, 2, 3])
 def test_vadd_unaligned_device_args(off):
     n = 10007
