@@ -50,6 +50,17 @@ for (hh, ww) in ((70, 132), (45, 77)):
     g.add_task(J.JACC_OP_CONV2D_F32, [g.a(ext, R), g.a(f, R), g.a(ob, W)], jacc.jacc_conv2d_params_t(hh, ww, 2, J.JACC_CONV2D_HALO_ROWS))
 bins_rw = np.ones(256, np.int32)
 g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(keys, R), g.a(bins_rw, RW)], jacc.jacc_hist_params_t(256))
+# round 2 (later): the 256-bit vadd (>= 2^26 elements, ragged tail), Black-Scholes
+# through its 256-bit (graph copies) and 128-bit (16-byte aligned view) kernels,
+# corr with 16-bit split partials (bits2 above) and 32-bit ones (2^20 documents)
+import torch
+nv = (1 << 26) + 5
+va = torch.rand(nv, device="cuda"); vb = torch.rand(nv, device="cuda"); vc = torch.empty(nv, device="cuda")
+g.add_task(J.JACC_OP_VADD_F32, [g.a(va, R), g.a(vb, R), g.a(vc, W)])
+ub = torch.rand(n + 8, device="cuda"); cb = torch.zeros(n + 8, device="cuda"); pb = torch.zeros(n + 8, device="cuda")
+g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(ub[4:4 + n], R), g.a(cb[4:4 + n], W), g.a(pb[4:4 + n], W)])
+bits3 = synth.corr_bitsets(100, 1 << 20); cc3 = np.zeros((100, 100), np.int32)
+g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits3.view(np.int32), R), g.a(bits3.view(np.int32), R), g.a(cc3, W)], jacc.jacc_corr_params_t(100, 100, 1 << 15))
 g.run(); g.run()
 print("ok", g.stats()["launches"])
 g.destroy()
