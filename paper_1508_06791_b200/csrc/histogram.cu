@@ -12,11 +12,15 @@
 //     bin%2.  A lane's word always sits in bank `lane`, so the 32 updates of
 //     a warp never conflict, for ANY key distribution (uniform or all-equal);
 //     the update is a shared-memory atomic add whose result is unused (no
-//     dependency chain between a lane's keys).
+//     dependency chain between a lane's keys).  Two warps share each
+//     sub-histogram (lane l of both: still bank l), which halves the shared
+//     memory per warp and lets 16 warps per SM stream keys instead of 12.
 //   * keys stream in as 128-bit loads, 8 int4 per lane per chunk, with the
 //     next chunk prefetched into registers while the current one is counted.
-//   * before a 16-bit counter can overflow (<= 65504 keys per lane) the warp
-//     folds its sub-histograms into per-lane 32-bit register totals (lane l
+//   * before a 16-bit counter can overflow (every 1023 chunks of the pair:
+//     <= 65472 keys per lane counter; both warps run the same trip count and
+//     meet at a pair barrier) one warp of the pair folds the sub-histogram
+//     into per-lane 32-bit register totals (lane l
 //     owns bins 8l..8l+7; column reads are rotated so they stay
 //     conflict-free) and clears them (an 8-bit form had to fold every 240
 //     keys: 184 vs 182 us at 2^28);
@@ -41,17 +45,22 @@ namespace jacc_k {
 namespace {
 
 // 16-bit lane-private counters: word (bin/2)*32 + lane, half bin%2 -- 16 KB
-// per warp, so 4 warps per block (3 blocks / SM); a lane flushes only every
-// 4095 chunks (65520 keys) instead of every 240 keys, which removes the
-// 8-bit form's fold (64 shared loads + 64 stores + ~4 ALU ops per word per
-// 240 keys: ~0.5 shared-memory op and ~1 ALU op per key).
+// per sub-histogram, SHARED by the two warps of a pair (lane l of both warps
+// owns bank l, so the sharing adds no bank conflict): 2 sub-histograms per
+// 4-warp block, 4 blocks (16 warps) per SM.  One sub-histogram per warp
+// capped the SM at 12 warps (16.5 KB each): 181 -> 168 us at 2^28 keys.
+// A counter is folded before it can overflow -- every 1023 chunks of the
+// pair (2 x 1023 x 32 = 65472 keys per lane counter) instead of every 240
+// keys of the 8-bit form (whose fold cost ~0.5 shared op + ~1 ALU op per key).
 constexpr int kWarps16 = 4;
 constexpr int kBlock16 = kWarps16 * 32;
 constexpr int kU16 = 8;                    // int4 per lane per chunk (32 keys)
 constexpr int kChunk16 = 32 * kU16;
-constexpr int kFlush16 = 2047;             // 2047 * 32 = 65504 keys <= 65535 per lane
 constexpr int kSubWords16 = 129 * 32;      // 256 bins / 2 per word + 1 dummy group, x 32 lanes
-constexpr int kSmemBytes16 = kWarps16 * kSubWords16 * 4 + 256 * 4;
+constexpr int kShare = 2;                  // warps per sub-histogram (lane l of each writes bank l)
+constexpr int kFoldPair = 1023;            // 2 warps x 1023 chunks x 32 keys <= 65535 per lane counter
+constexpr int kBlocksPerSm16 = 4;          // 34 KB of shared memory, 128 registers per thread
+constexpr int kSmemBytes16 = (kWarps16 / kShare) * kSubWords16 * 4 + 256 * 4;
 
 __device__ __forceinline__ void count_key16(unsigned *sub_lane_w, int k, unsigned nbins) {
     const unsigned kk = min((unsigned)k, nbins);
@@ -92,16 +101,17 @@ __global__ void __launch_bounds__(kBlock16) hist256_w16_kernel(const int4 *__res
                                                                unsigned *__restrict__ acc, int assign, PeerOp pop) {
     extern __shared__ unsigned smem[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned *sub = smem + warp * kSubWords16;
-    unsigned *blockh = smem + kWarps16 * kSubWords16;
-    for (int g = 0; g < 129; ++g) sub[g * 32 + lane] = 0u;
+    unsigned *sub = smem + (warp / kShare) * kSubWords16;
+    unsigned *blockh = smem + (kWarps16 / kShare) * kSubWords16;
+    if (warp % kShare == 0)
+        for (int g = 0; g < 129; ++g) sub[g * 32 + lane] = 0u;
     for (int i = threadIdx.x; i < 256; i += kBlock16) blockh[i] = 0u;
     __syncthreads();
     unsigned tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t nwarps = (int64_t)gridDim.x * kWarps16;
-    int64_t c = (int64_t)blockIdx.x * kWarps16 + warp;
+    const int64_t c0 = (int64_t)blockIdx.x * kWarps16 + warp;
     const int64_t nchunks = (n4 + kChunk16 - 1) / kChunk16;
-    int since_flush = 0;
+    const int64_t trips = (nchunks + nwarps - 1) / nwarps;   // the same for every warp (pair barriers)
     int4 cur[kU16], nxt[kU16];
     auto load = [&](int64_t ch, int4 *dst) {
         if ((ch + 1) * kChunk16 <= n4) {
@@ -115,19 +125,24 @@ __global__ void __launch_bounds__(kBlock16) hist256_w16_kernel(const int4 *__res
             }
         }
     };
-    if (c < nchunks) load(c, cur);
-    for (; c < nchunks; c += nwarps) {
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / kShare), "n"(32 * kShare) : "memory"); };
+    if (c0 < nchunks) load(c0, cur);
+    for (int64_t k = 0; k < trips; ++k) {
+        const int64_t c = c0 + k * nwarps;
         load(c + nwarps, nxt);
+        if (c < nchunks) {
 #pragma unroll
-        for (int u = 0; u < kU16; ++u) {
-            count_key16(sub + lane, cur[u].x, nbins);
-            count_key16(sub + lane, cur[u].y, nbins);
-            count_key16(sub + lane, cur[u].z, nbins);
-            count_key16(sub + lane, cur[u].w, nbins);
+            for (int u = 0; u < kU16; ++u) {
+                count_key16(sub + lane, cur[u].x, nbins);
+                count_key16(sub + lane, cur[u].y, nbins);
+                count_key16(sub + lane, cur[u].z, nbins);
+                count_key16(sub + lane, cur[u].w, nbins);
+            }
         }
-        if (++since_flush == kFlush16) {
-            flush16(sub, lane, tot);
-            since_flush = 0;
+        if ((k + 1) % kFoldPair == 0) {
+            pair_sync();
+            if (warp % kShare == 0) flush16(sub, lane, tot);
+            pair_sync();
         }
 #pragma unroll
         for (int u = 0; u < kU16; ++u) cur[u] = nxt[u];
@@ -138,7 +153,8 @@ __global__ void __launch_bounds__(kBlock16) hist256_w16_kernel(const int4 *__res
             if ((unsigned)k < (unsigned)nbins) atomicAdd(&blockh[k], 1u);
         }
     }
-    flush16(sub, lane, tot);
+    pair_sync();
+    if (warp % kShare == 0) flush16(sub, lane, tot);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -198,9 +214,11 @@ cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbi
     }
     int grid, block;
     if (nbins <= 256) {
-        // 16-bit lane counters, 4 warps x 66 KB per block, 3 blocks per SM
-        // (measured at 2^28: 182 us vs 184 for the 8-bit form; prefetching 2
-        // or 3 chunks ahead instead of 1: 186 / 223 us)
+        // 16-bit lane counters shared by warp pairs: 4 warps and 34 KB per
+        // block, 4 blocks per SM (measured at 2^28: 168 us; one sub-histogram
+        // per warp, 3 blocks per SM: 182; the 8-bit form 184; the per-warp
+        // form prefetching 2 or 3 chunks ahead 186 / 223; with 6 blocks per SM
+        // at <= 80 registers 193 (spills))
         auto kern = pop ? hist256_w16_kernel<true> : hist256_w16_kernel<false>;
         cudaError_t e = set_max_dyn_smem((const void *)kern, kSmemBytes16);
         if (e != cudaSuccess) return e;
@@ -211,7 +229,7 @@ cudaError_t histogram_i32(const int32_t *keys, int64_t n, int32_t *bins, int nbi
         const int64_t n4 = (n - head) / 4;
         const int64_t tail0 = head + 4 * n4;
         const int64_t nchunks = (n4 + kChunk16 - 1) / kChunk16;
-        pick_grid(s, (nchunks + kWarps16 - 1) / kWarps16, 3, kBlock16, &grid, &block);
+        pick_grid(s, (nchunks + kWarps16 - 1) / kWarps16, kBlocksPerSm16, kBlock16, &grid, &block);
         block = kBlock16;
         int64_t edge_head = head;
         if (head > 0 && tail0 < n) {

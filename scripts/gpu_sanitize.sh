@@ -61,6 +61,8 @@ ub = torch.rand(n + 8, device="cuda"); cb = torch.zeros(n + 8, device="cuda"); p
 g.add_task(J.JACC_OP_BLACKSCHOLES_F32, [g.a(ub[4:4 + n], R), g.a(cb[4:4 + n], W), g.a(pb[4:4 + n], W)])
 bits3 = synth.corr_bitsets(100, 1 << 20); cc3 = np.zeros((100, 100), np.int32)
 g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits3.view(np.int32), R), g.a(bits3.view(np.int32), R), g.a(cc3, W)], jacc.jacc_corr_params_t(100, 100, 1 << 15))
+bits4 = synth.corr_bitsets(1536, 4096); cc4 = np.zeros((1536, 1536), np.int32)   # the CTA-pair corr kernel, (2, 1, 2) clusters
+g.add_task(J.JACC_OP_CORR_POPC_U32, [g.a(bits4.view(np.int32), R), g.a(bits4.view(np.int32), R), g.a(cc4, W)], jacc.jacc_corr_params_t(1536, 1536, 128))
 g.run(); g.run()
 print("ok", g.stats()["launches"])
 g.destroy()

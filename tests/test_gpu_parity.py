@@ -235,6 +235,24 @@ def test_hist_unaligned_and_accumulate(off, n, mode):
     g.destroy()
 
 
+@pytest.mark.parametrize("dist", ["zeros", "uniform", "with_out_of_range"])
+def test_hist_counter_fold(dist):
+    """The 16-bit lane counters' in-loop fold (before a counter can overflow):
+    one block of 4 warps (advisory schedule) over 2^23 + 12345
+    keys gives every warp > 2047 chunks of 32 keys per lane -- all keys in
+    one bin loads a single counter to its limit before the fold."""
+    n = (1 << 23) + 12345
+    keys = synth.hist_keys(n, 256, seed=5, dist=dist)
+    dk = _dev(keys)
+    db = torch.zeros(256, dtype=torch.int32, device="cuda")
+    g = _graph()
+    g.add_task(J.JACC_OP_HISTOGRAM_I32, [g.a(dk, R), g.a(db, W)], jacc.jacc_hist_params_t(256),
+               sched=jacc.jacc_schedule_t((128, 0, 0), (128, 0, 0), 0))
+    g.run()
+    assert np.array_equal(db.cpu().numpy(), oracle.histogram(keys, 256))
+    g.destroy()
+
+
 def test_hist_full_size_config2():
     """BASELINE config 2 size (2^28 keys), the launch configuration bench.py times."""
     keys = synth.hist_keys()
