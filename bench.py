@@ -926,7 +926,7 @@ def cfg1_latency(torch, J, reps=200):
     ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
     tc, ts = torch.empty(a.size, pin_memory=True), torch.empty(1, pin_memory=True)
     colds = []
-    for trial in range(3):   # cold = first execute of a FRESH graph (plan, device copies, copies)
+    for trial in range(5):   # cold = first execute of a FRESH graph (plan, device copies, copies)
         g, _ = make_graph(torch.cuda.current_device(), n_streams=2, flags=J.JACC_GRAPH_MERGE)
         g.add_task(J.JACC_OP_VADD_F32, [g.a(ta, R, True), g.a(tb, R, True), g.a(tc, W)])
         g.add_task(J.JACC_OP_REDUCE_SUM_F32, [g.a(tc, R), g.a(ts, W)])
@@ -934,9 +934,14 @@ def cfg1_latency(torch, J, reps=200):
         t0 = time.perf_counter()
         g.run()
         colds.append((time.perf_counter() - t0) * 1e6)
-        if trial < 2:
+        if trial < 4:
             g.destroy()
+    # host wall clock of a first execute: its device allocations go through
+    # torch's caching allocator on fresh streams (~0.7 ms of cudaMalloc in a
+    # quiet process, JACC_LOG=1), and single trials on the shared boxes have
+    # ranged up to tens of ms -- the median of 5 and the best are reported
     out["e2e_cold_us"] = statistics.median(colds)
+    out["e2e_cold_best_us"] = min(colds)
     out["e2e_cold_trials_us"] = colds
     out["e2e_warm_cachable_us"] = _median_run_us(g, reps)
     st = g.stats()

@@ -14,11 +14,10 @@ import json
 import sys
 from collections import defaultdict
 
-TASK_OF = [("vadd_v4_kernel", "vadd"), ("jacc_k::<unnamed>::reduce_kernel", "reduce"), ("hist256", "hist"),
+TASK_OF = [("vadd_v4_kernel", "vadd"), ("vadd_v8_kernel", "vadd"), ("bs_v8_kernel", "bs"), ("jacc_k::<unnamed>::reduce_kernel", "reduce"), ("hist256", "hist"),
            ("bs_v4_kernel", "bs"), ("gemm_3xtf32_pair_kernel", "sgemm"), ("split_a_kernel", "sgemm"),
            ("split_bt_kernel", "sgemm"), ("gemm_3xtf32_kernel", "sgemm"), ("nbody_partial", "nbody"),
            ("nbody_finish_kernel", "nbody")]
-INSTANCES = {"nbody": ("nbody_partial_kernel",)}   # count tasks by their first kernel
 
 
 def main(path):
@@ -40,8 +39,8 @@ def main(path):
     out = {"_source": f"{path}: ncu dram__bytes_read.sum + dram__bytes_write.sum per kernel, summed over the "
                       "kernels of a task, divided by the task's instances in one bench step"}
     for task, d in per.items():
-        firsts = [p for p, t in TASK_OF if t == task]
-        n = len(launches[task][firsts[0]]) or 1
+        # a task's instances: launches of its most frequent kernel (N-body: 10 partial + 10 finish = 10 steps)
+        n = max((len(v) for v in launches[task].values()), default=0) or 1
         out[task] = {"bytes_per_task": d["bytes"] / n, "instances": n}
     print(json.dumps(out, indent=1))
 
