@@ -333,14 +333,21 @@ def kernel_report(times, units, peaks, clocks_mhz=None):
     traffic = _traffic()
     for name in out:
         out[name]["traffic"] = traffic.get(name)
-    # the memory roof of each HBM task's own read/write mix (scripts/micro/stream_mix.cu, profiles/)
+    # the memory roof of each HBM task's own read/write mix, the best plain
+    # stream of that mix measured by the micro-benchmarks (profiles/
+    # stream_shape.json: access width and depth; stream_mix.json: the 128-bit
+    # loader).  Read-only tasks have none: at 2^26 floats the micro's read
+    # stream is launch-bound (5.5 TB/s) and the best read stream measured is
+    # the reduction's own (6.73 TB/s at 2^28), so the copy figure stays theirs.
     try:
+        shape = json.load(open(os.path.join(ROOT, "profiles", "stream_shape.json")))["GBps"]
         mix = json.load(open(os.path.join(ROOT, "profiles", "stream_mix.json")))
-        for name, key in (("bs", "read1_write2"), ("hist", "read_only"), ("vadd", "read2_write1"),
-                          ("reduce", "read_only")):
+        roof = {"read1_write2": max([v for k, v in shape.items() if k.startswith("R1W2")] + [mix["read1_write2"]]),
+                "read2_write1": mix["read2_write1"]}
+        for name, key in (("bs", "read1_write2"), ("vadd", "read2_write1")):
             if name in out and "achieved" in out[name]:
-                out[name]["mix_stream_GBps"] = mix[key]
-                out[name]["frac_of_mix_stream"] = out[name]["achieved"] / mix[key]
+                out[name]["mix_stream_GBps"] = roof[key]
+                out[name]["frac_of_mix_stream"] = out[name]["achieved"] / roof[key]
     except Exception:
         pass
     # N-body against the measured paired-FP32 ceiling (scripts/micro/fp32_pipes.cu, profiles/): 11 paired
