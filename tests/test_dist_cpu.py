@@ -1,4 +1,4 @@
-"""Multi-process (world_size 2, gloo, CPU) checks of the N>1 path's host logic.
+"""Multi-process (world_size 2 and 4, gloo, CPU) checks of the N>1 path's host logic.
 
 The GPU box used here has one GPU, so the SPMD decomposition bench.py uses at
 N>1 is verified on CPU: every rank takes its shard
@@ -6,7 +6,7 @@ N>1 is verified on CPU: every rank takes its shard
 the same collective the GPU path issues through NCCL (allreduce of partial
 sums / bins, allgather of N-body positions).  The combination must equal the
 single-process oracle -- bitwise where §8(e) says so -- and each rank's
-libjacc.so plan (built with world = 2) must have the counted copies of the
+libjacc.so plan (built with world = 2 / 4) must have the counted copies of the
 SURVEY count table.
 """
 import os
@@ -135,9 +135,9 @@ def _worker(rank, world, port, q):
         q.put((rank, {"error": traceback.format_exc()}))
 
 
-def test_spmd_world2_gloo():
-    world = 2
-    port = 29500 + (os.getpid() % 1000)
+@pytest.mark.parametrize("world", [2, 4])
+def test_spmd_gloo(world):
+    port = 29500 + (os.getpid() % 1000) + 7 * world
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
