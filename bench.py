@@ -785,7 +785,9 @@ def hist_kiter_spmd(torch, J, dist, rank, world, comm_ptr, p2p, red_dev, K=400):
     g, _ = make_graph(torch.cuda.current_device(), n_streams=2, rank=rank, world=world,
                       nccl_comm=0 if p2p else comm_ptr, flags=flags)
     if p2p:
-        peer_setup(g, 8 << 20)
+        # every allreduce task owns its staging: 2 epochs x world rows of 256
+        # bins as 8-byte {value, epoch} words (peer.cuh allreduce_stage_bytes)
+        peer_setup(g, K * 2 * 256 * 8 * world + (4 << 20))
     n = 1 << 24
     lo, hi = synth.shard_range(n, rank, world)
     keys = torch.from_numpy(synth.hist_keys(n)[lo:hi]).cuda()
