@@ -204,7 +204,7 @@ def _worker(rank, world, port, q):
         q.put((rank, {"error": traceback.format_exc()}))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_p2p_world2_one_gpu(world):
     """world ranks = world processes time-sliced on the box's one GPU."""
     import torch.multiprocessing as mp
@@ -348,7 +348,7 @@ def _halo_worker(rank, world, port, q, cases):
         q.put((rank, {"error": traceback.format_exc()}))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_p2p_conv2d_row_bands(world):
     """Every rank's halo rows equal oracle.halo_band and its output rows equal
     the single-GPU convolution of the whole image bit for bit (same kernel,
